@@ -1,0 +1,404 @@
+#!/usr/bin/env python3
+"""bench.py — BML step throughput on B200 (Gcell-updates/s), one JSON line on rank 0.
+
+Metric (BASELINE.json): Gcell-updates/sec and % of HBM roofline vs the host-CPU
+reference. 1 cell-update = one cell advanced by one full BML step (LR + TB phase).
+
+A bench "step" = one reference-style run(): `steps` full BML steps of the whole
+N x N lattice (the unit the reference's own `bml bench` times, tools/main.cpp:195-201).
+Default workload = BASELINE configs[1]: N=1024, rho=0.38, 4096 steps, seed 1.
+
+  value     device-resident throughput: lattice already in HBM, CUDA events on the
+            launching stream around each bench step, L2 flushed (256 MiB write)
+            between bench steps outside the events.
+  e2e       the same through the C-ABI (include/bml_dev.h) with pinned HOST
+            buffers: upload (H2D) + steps + download (D2H) per bench step.
+  roofline  dominant kernel (step_block_kernel): algorithmic bytes 4 B per
+            cell-update / its average launch time, vs the
+            measured HBM copy bandwidth in MEASURED_PEAKS.json.
+  cpu_baseline  the unmodified reference (oracle/_ref/ref_driver, its own bench
+            method) on this host, bounded sample, rank 0 only.
+
+--impl reference runs only the reference CPU implementation (best of `lanes` 1
+thread and `parallel` with all host threads) and prints the same line shape.
+"""
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+
+WORKLOADS = {
+    # name: (n, rho, seed, steps, description)
+    "c0": (256, 0.3, 1, 1024, "configs[0]: N=256 rho=0.3 1024 steps"),
+    "c1": (1024, 0.38, 1, 4096, "configs[1]: N=1024 rho=0.38 4096 steps"),
+    "c2ff": (8192, 0.25, 1, 10000, "configs[2]: N=8192 rho=0.25 10000 steps"),
+    "c2jam": (8192, 0.5, 1, 10000, "configs[2]: N=8192 rho=0.5 10000 steps"),
+    "c3": (32768, 0.35, 1, 10000, "configs[3]: N=32768 rho=0.35 10000 steps"),
+    "c4": (65536, 0.35, 1, 10000, "configs[4]: N=65536 rho=0.35 10000 steps"),
+}
+BYTES_PER_CELL_UPDATE = 4  # 1 B read + 1 B write per cell per phase
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- C-ABI (ctypes)
+def load_abi():
+    import paper_1804_07981_b200 as bml
+
+    lib = ctypes.CDLL(bml.LIB_DEV)
+    vp = ctypes.c_void_p
+    lib.bml_dev_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
+    lib.bml_dev_destroy.argtypes = [vp]
+    lib.bml_dev_upload.argtypes = [vp, vp, ctypes.c_size_t]
+    lib.bml_dev_download.argtypes = [vp, vp, ctypes.c_size_t]
+    lib.bml_dev_step.argtypes = [vp, ctypes.c_int64, vp, vp, vp, vp]
+    lib.bml_dev_set_stream.argtypes = [vp, vp]
+    lib.bml_dev_sync.argtypes = [vp]
+    lib.bml_dev_configure.argtypes = [vp, ctypes.c_int, ctypes.c_int]
+    lib.bml_dev_enable_timing.argtypes = [vp, ctypes.c_int]
+    lib.bml_dev_kernel_stats.argtypes = [vp, ctypes.POINTER(ctypes.c_int64),
+                                         ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+    lib.bml_dev_info.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 5 + [ctypes.POINTER(ctypes.c_size_t)]
+    lib.bml_dev_last_error.restype = ctypes.c_char_p
+    return lib
+
+
+def abi_check(lib, rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what} failed rc={rc}: {lib.bml_dev_last_error().decode()}")
+
+
+# ---------------------------------------------------------------- reference CPU arm
+def ref_bench(n, rho, seed, steps, backend, threads, reps):
+    out = subprocess.run([REF_DRIVER, "bench", f"n={n}", f"rho={rho}", f"seed={seed}",
+                          f"steps={steps}", f"backend={backend}", f"threads={threads}",
+                          f"reps={reps}"], check=True, capture_output=True, text=True)
+    rec = json.loads(out.stdout)
+    rec["gcups"] = n * n * steps / rec["mean_s"] / 1e9
+    return rec
+
+
+def cpu_sample_plan(n, steps):
+    """Bounded samples (~seconds each) of the same workload for the CPU arms."""
+    cells = n * n
+    lanes_steps = max(1, min(steps, int(6e9 / cells)))      # ~1-3 s at 2-6 Gcell/s
+    par_steps = max(1, min(steps, int(1.5e9 / cells)))      # scalar kernel, all threads
+    return lanes_steps, par_steps
+
+
+def reference_arm(n, rho, seed, steps, reps):
+    if not os.path.exists(REF_DRIVER):
+        return None, "oracle/_ref/ref_driver not built"
+    lanes_steps, par_steps = cpu_sample_plan(n, steps)
+    lanes = ref_bench(n, rho, seed, lanes_steps, "lanes", 1, reps)
+    par = ref_bench(n, rho, seed, par_steps, "parallel", 0, reps)
+    best = lanes if lanes["gcups"] >= par["gcups"] else par
+    return {"lanes": lanes, "parallel": par, "best": best}, None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference_impl(args, wl):
+    n, rho, seed, steps, desc = wl
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    reps = max(1, args.steps)
+    res, err = reference_arm(n, rho, seed, steps, reps)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": err}))
+        return
+    best = res["best"]
+    value = best["gcups"]
+    line = {
+        "impl": "reference",
+        "metric": "Gcell-updates/sec",
+        "value": value,
+        "unit": "Gcell-updates/s",
+        "n_gpus": args.gpus,
+        "steps": reps,
+        "warmup": 0,
+        "ms_per_step": best["mean_s"] * 1e3 * steps / best["steps"],
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic (reference init_grid seed)",
+        "config": {"workload": desc, "n": n, "rho": rho, "seed": seed, "steps_per_run": steps},
+        "cpu_baseline": {
+            "value": value, "unit": "Gcell-updates/s", "cores": best["threads"],
+            "kind": "reference",
+            "sample": (f"{best['backend']} backend, {best['steps']} of {steps} steps per rep, "
+                       f"{reps} reps, reference bench method (tools/main.cpp:195-214)"),
+            "host": cpu_model(), "hardware_concurrency": best["hardware_concurrency"],
+            "lane_width": best["lane_width"],
+            "lanes_1thread_gcups": res["lanes"]["gcups"],
+            "parallel_all_threads_gcups": res["parallel"]["gcups"],
+            "parallel_threads": res["parallel"]["threads"],
+        },
+        "e2e": {"value": value, "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------- b200 arm
+def run_b200(args, wl):
+    import torch
+    import paper_1804_07981_b200 as bml
+
+    n, rho, seed, steps, desc = wl
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        return run_b200_multi(args, wl)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    grid = bml.init_grid(n, rho, seed)  # reference RNG path (untimed input generation)
+    lat = bml.DeviceLattice(n)
+    lat.configure(block_steps=args.block, strip_rows=args.strip)
+    stream = torch.cuda.Stream(device=dev)
+    lat.set_stream(stream.cuda_stream)
+    lat.upload(grid)
+    abi = load_abi()
+    h = ctypes.c_void_p(lat.handle())
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    # warm-up
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            lat.step(steps)
+    stream.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    abi_check(abi, abi.bml_dev_enable_timing(h, 1), "enable_timing")
+    abi_check(abi, abi.bml_dev_kernel_stats(h, None, None, 1), "kernel_stats reset")
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.fill_(i & 0xFF)  # evict the lattice from L2 between bench steps
+                starts[i].record(stream)
+                lat.step(steps)
+                ends[i].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    launches = ctypes.c_int64()
+    kms = ctypes.c_double()
+    abi_check(abi, abi.bml_dev_kernel_stats(h, ctypes.byref(launches), ctypes.byref(kms), 1),
+              "kernel_stats")
+    abi_check(abi, abi.bml_dev_enable_timing(h, 0), "enable_timing")
+    per_step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(per_step_ms)
+    cell_updates = n * n * steps * args.steps
+    value = cell_updates / (total_ms / 1e3) / 1e9
+
+    peak, peak_src = measured_peaks()
+    avg_launch_ms = kms.value / max(1, launches.value)
+    bytes_per_launch = BYTES_PER_CELL_UPDATE * n * n * steps * args.steps / max(1, launches.value)
+    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    kernel_share = kms.value / total_ms if total_ms else None
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    # e2e through the C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(abi, torch, bml, grid, n, steps, args)
+
+    cpu = None
+    if not args.no_cpu and rank == 0:
+        res, err = reference_arm(n, rho, seed, steps, 3)
+        if res:
+            best = res["best"]
+            cpu = {"value": best["gcups"], "unit": "Gcell-updates/s", "cores": best["threads"],
+                   "kind": "reference",
+                   "sample": (f"{best['backend']} backend, {best['steps']} of {steps} steps x 3 reps, "
+                              "reference bench method (tools/main.cpp:195-214)"),
+                   "host": cpu_model(),
+                   "lanes_1thread_gcups": res["lanes"]["gcups"],
+                   "parallel_all_threads_gcups": res["parallel"]["gcups"],
+                   "parallel_threads": res["parallel"]["threads"]}
+        else:
+            cpu = {"value": None, "unavailable": err}
+
+    line = {
+        "metric": "Gcell-updates/sec",
+        "value": value,
+        "unit": "Gcell-updates/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic: reference init_grid(n, rho, seed) lattice",
+        "config": {"workload": desc, "n": n, "rho": rho, "seed": seed, "steps_per_run": steps,
+                   "parallelism": "single GPU", "l2": "flushed (256 MiB write) between bench steps",
+                   "block_steps": args.block, "strip_rows": args.strip,
+                   "layout": "bit-planes, 2 bits/cell"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "step_block_kernel", "peak_source": peak_src,
+                     "algorithmic_bytes_per_cell_update": BYTES_PER_CELL_UPDATE,
+                     "launches": launches.value, "avg_launch_us": avg_launch_ms * 1e3,
+                     "kernel_share_of_step": kernel_share},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches.value,
+        "wall_s": wall,
+        "clocks": clocks.summary(),
+        "gpu": torch.cuda.get_device_name(dev),
+    }
+    print(json.dumps(line))
+
+
+def run_e2e(abi, torch, bml, grid, n, steps, args):
+    vp = ctypes.c_void_p
+    h = vp()
+    abi_check(abi, abi.bml_dev_create(n, torch.cuda.current_device(), ctypes.byref(h)), "create")
+    try:
+        abi_check(abi, abi.bml_dev_configure(h, args.block, args.strip), "configure")
+        host_in = torch.frombuffer(bytearray(grid.to_bytes()), dtype=torch.uint8).pin_memory()
+        host_out = torch.empty(n * n, dtype=torch.uint8).pin_memory()
+        for _ in range(max(1, args.warmup)):
+            abi_check(abi, abi.bml_dev_upload(h, vp(host_in.data_ptr()), n), "upload")
+            abi_check(abi, abi.bml_dev_step(h, steps, None, None, None, None), "step")
+            abi_check(abi, abi.bml_dev_download(h, vp(host_out.data_ptr()), n), "download")
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            abi_check(abi, abi.bml_dev_upload(h, vp(host_in.data_ptr()), n), "upload")
+            abi_check(abi, abi.bml_dev_step(h, steps, None, None, None, None), "step")
+            abi_check(abi, abi.bml_dev_download(h, vp(host_out.data_ptr()), n), "download")
+            times.append(time.perf_counter() - t0)
+        # correctness of what was timed: the device result equals the public API's
+        final = bml.step(grid, steps)
+        assert bytes(host_out.numpy()) == final.to_bytes(), "e2e result mismatch"
+        total = sum(times)
+        return {"value": n * n * steps * len(times) / total / 1e9, "unit": "Gcell-updates/s",
+                "h2d_bytes_per_step": n * n, "d2h_bytes_per_step": n * n,
+                "ms_per_step": total / len(times) * 1e3,
+                "path": "C-ABI bml_dev_upload/step/download, pinned host buffers"}
+    finally:
+        abi.bml_dev_destroy(h)
+
+
+def run_b200_multi(args, wl):
+    raise SystemExit("multi-GPU bench: see bench_multi in a later revision")
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c1")
+    ap.add_argument("--block", type=int, default=16)
+    ap.add_argument("--strip", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_impl(args, wl)
+    else:
+        run_b200(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/* include/bml_dev.h — C-ABI of the B200-native BML (Biham–Middleton–Levine) step.
+ *
+ * This is the drop-in boundary: the reference C++ API (namespace bml, SURVEY.md
+ * §8(b)) is re-implemented on the host in paper_1804_07981_b200/csrc/host/ and
+ * reaches the GPU only through these functions. Plain pointers and sizes, no
+ * torch or C++ types. All functions return a status code:
+ *
+ *   BML_OK      0  success
+ *   BML_EINVAL  1  invalid argument   (reference: std::invalid_argument)
+ *   BML_ECUDA   2  CUDA / peer error  (reference: none — new failure mode)
+ *   BML_ENOMEM  3  device allocation failed
+ *   BML_ECONSERVE 4 per-step vehicle conservation violated
+ *                   (reference: std::logic_error, src/engine.cpp:219-224)
+ *
+ * bml_dev_last_error() returns a thread-local message for the last failure.
+ * A handle is not thread-safe; one host thread drives it.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/proj):
+ *   bml_dev_create        GridPair make_grid_pair(Backend, const Grid&)   include/bml/engine.hpp:60
+ *                         (allocation half: the device-resident double buffer)
+ *   bml_dev_upload        make_grid_pair's interior copy                   src/engine.cpp:59-64, src/grid.cpp:37-49
+ *   bml_dev_init_random   Grid init_grid(const SeedSpec&)                  include/bml/seeding.hpp:42
+ *   bml_dev_phase         void step_phase(Backend, GridPair&, Phase, int)  include/bml/engine.hpp:66
+ *   bml_dev_step          void step(Backend, GridPair&, int) x steps,      include/bml/engine.hpp:70
+ *                         and the loops of Grid run(...)                   src/engine.cpp:206-235
+ *                         with moved_in_phase / count_vehicles fused       src/metrics.cpp:8-29
+ *   bml_dev_counts        VehicleCounts count_vehicles(const Grid&)        include/bml/metrics.hpp:20
+ *   bml_dev_download      readback: Grid::interior / data                  include/bml/grid.hpp:38-47
+ *   bml_dev_destroy       ~GridPair
+ *
+ * Lattice bytes crossing this boundary use the reference cell encoding
+ * (include/bml/cell.hpp:9): 0 = Empty, 1 = LR, 2 = TB. On the device the
+ * lattice is bit-sliced (two bit planes, 32 cells per word); see DESIGN.md.
+ */
+#ifndef BML_DEV_H
+#define BML_DEV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BML_OK 0
+#define BML_EINVAL 1
+#define BML_ECUDA 2
+#define BML_ENOMEM 3
+#define BML_ECONSERVE 4
+
+#define BML_PHASE_HORIZONTAL 0 /* bml::Phase::Horizontal — LR vehicles move right */
+#define BML_PHASE_VERTICAL 1   /* bml::Phase::Vertical   — TB vehicles move down  */
+
+typedef struct bml_dev bml_dev;
+
+/* Number of visible CUDA devices. */
+int bml_dev_device_count(int *count);
+
+/* Allocate a device-resident n x n torus on CUDA device `device` (-1 = the
+ * calling thread's current device); the whole lattice is one row band. */
+int bml_dev_create(int n, int device, bml_dev **out);
+
+/* Allocate rows [row_begin, row_end) of an n x n torus as one row band on
+ * `device` (multi-GPU decomposition). The band exchanges
+ * halo rows with its two neighbours after bml_dev_connect(). */
+int bml_dev_create_band(int n, int row_begin, int row_end, int device, bml_dev **out);
+
+int bml_dev_destroy(bml_dev *dev);
+
+/* Copy the band's rows in from host (or device) memory: `src` points at cell
+ * (row_begin, 0); consecutive rows are `src_pitch` bytes apart. A halo-layout
+ * reference Grid passes data()+stride+1 with pitch n+2. Cells must be 0/1/2. */
+int bml_dev_upload(bml_dev *dev, const uint8_t *src, size_t src_pitch);
+
+/* Copy the band's rows out, same addressing as bml_dev_upload. */
+int bml_dev_download(bml_dev *dev, uint8_t *dst, size_t dst_pitch);
+
+/* Fill the lattice exactly as the reference init_grid({n, rho, seed}) does
+ * (SplitMix64 + descending Fisher–Yates), computed on the device.
+ * Single-band handles only. */
+int bml_dev_init_random(bml_dev *dev, double rho, uint64_t seed);
+
+/* One phase (step_phase). `moved` (nullable) receives the vehicles that
+ * advanced (moved_in_phase). Single-band handles only. */
+int bml_dev_phase(bml_dev *dev, int phase, int64_t *moved);
+
+/* `steps` full steps (LR phase then TB phase each). Each of the four metric
+ * arrays is nullable; when any is non-NULL, all requested arrays (length
+ * `steps`) receive the per-step values of the reference observer loop
+ * (engine.cpp:211-235): lr_moved, tb_moved, and the post-step lr/tb counts.
+ * With counts requested, conservation is checked each step and a violation
+ * returns BML_ECONSERVE. For bands, the values are this band's share. */
+int bml_dev_step(bml_dev *dev, int64_t steps, int64_t *lr_moved, int64_t *tb_moved,
+                 int64_t *lr_count, int64_t *tb_count);
+
+/* Vehicle counts of the band's rows (count_vehicles). */
+int bml_dev_counts(bml_dev *dev, int64_t *lr, int64_t *tb);
+
+/* Launch on an external CUDA stream (cudaStream_t passed as void*; NULL
+ * restores the handle's own stream). Used by bench.py to time on the launching
+ * stream with CUDA events. */
+int bml_dev_set_stream(bml_dev *dev, void *stream);
+int bml_dev_sync(bml_dev *dev);
+
+/* Tuning knobs (0 = keep current): temporal block depth (full steps fused per
+ * launch, 1..16) and rows per strip. */
+int bml_dev_configure(bml_dev *dev, int block_steps, int strip_rows);
+
+/* Kernel statistics since the last reset: launches of the step kernels and
+ * their summed device time (CUDA events around each launch; enable first). */
+int bml_dev_enable_timing(bml_dev *dev, int enable);
+int bml_dev_kernel_stats(bml_dev *dev, int64_t *launches, double *kernel_ms, int reset);
+
+/* Geometry / introspection. */
+int bml_dev_info(bml_dev *dev, int *n, int *row_begin, int *row_end, int *block_steps,
+                 int *strip_rows, size_t *device_bytes);
+
+/* ---- multi-GPU plumbing (one process per GPU, or one process driving all) ----
+ * bml_dev_export() writes an opaque blob (CUDA IPC handles of the band's two
+ * lattice buffers and its halo flags) of at most BML_EXPORT_BYTES bytes.
+ * bml_dev_connect() maps the up-neighbour's (rows above, periodic) and
+ * down-neighbour's blobs. After connect, bml_dev_step() writes halo rows
+ * straight into the neighbours' buffers from inside the step kernel (NVLink
+ * peer stores) and signals them with system-scope flags; no NCCL on the data
+ * path. bml_dev_connect_local() does the same for handles living in this
+ * process (peer access instead of IPC). */
+#define BML_EXPORT_BYTES 512
+int bml_dev_export(bml_dev *dev, void *blob, size_t *size);
+int bml_dev_connect(bml_dev *dev, const void *up_blob, const void *down_blob);
+int bml_dev_connect_local(bml_dev *dev, bml_dev *up, bml_dev *down);
+
+/* Must be called on every band after upload/init and before the first step
+ * when bands are connected: publishes boundary rows into neighbour halos. */
+int bml_dev_exchange_halos(bml_dev *dev);
+
+const char *bml_dev_last_error(void);
+
+/* Library version / build string, e.g. "bml_dev 0.1.0 sm_100a". */
+const char *bml_dev_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BML_DEV_H */

@@ -1,0 +1,1135 @@
+// paper_1804_07981_b200/csrc/bml_dev.cu — B200-native BML lattice engine (sm_100a).
+//
+// Implements include/bml_dev.h. The reference (/root/reference/proj) keeps one
+// byte per cell and runs each phase as a separate pass (src/engine.cpp:68-120,
+// src/lanes.cpp:59-88). Here the lattice stays resident in HBM as two bit
+// planes (bit j of word w of row i: plane L = "LR vehicle", plane T = "TB
+// vehicle"), 32 cells per 32-bit word, the two planes interleaved as uint2.
+// That is 2 bits/cell instead of 8, and both phase rules become a handful of
+// LOP3/funnel-shift instructions per 32 cells:
+//
+//   LR phase (engine.hpp:32-36, lanes.cpp:52-57), on one row:
+//     E      = ~(L | T)                               empty cells
+//     prevL  = L shifted one cell right (cell j sees cell j-1), torus wrap
+//     nextE  = E shifted one cell left  (cell j sees cell j+1), torus wrap
+//     vacate = L & nextE                              moved_in_phase mask
+//     L'     = (prevL & E) | (L & ~nextE)
+//   TB phase (engine.hpp:38-42), rows i-1, i, i+1 after the LR phase:
+//     T'(i)  = (T(i-1) & E(i)) | (T(i) & ~E(i+1)),    vacate = T(i) & E(i+1)
+//
+// The step kernel (step_block_kernel) is temporally blocked: one warp walks
+// down a strip of rows, and K full steps (2K phases) are pipelined in
+// registers, so each launch reads the lattice once and writes it once for K
+// steps. Column wrap uses warp shuffles; each warp owns 30 output words plus
+// one halo word on each side (the dependency cone grows one cell per step,
+// K <= 32). Vertical wrap and band decomposition use kHalo ghost rows above
+// and below the band, which the kernel itself refreshes for the NEXT launch
+// (directly into a neighbour GPU's buffer over NVLink for row bands).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "bml_dev.h"
+
+namespace {
+
+constexpr int kHalo = 16;       // ghost rows per side == max steps fused per launch
+constexpr int kMaxBlock = 16;   // largest K instantiated
+constexpr int kWarpsPerCta = 4;
+constexpr int kOutWords = 30;   // output words per warp in the haloed modes
+constexpr unsigned kFull = 0xffffffffu;
+
+enum Mode { kGeneric = 0, kAligned = 1, kFullRow = 2 };
+
+// ---------------------------------------------------------------- error state
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    (void)cudaGetLastError();  // clear sticky-free errors
+    const int code = (e == cudaErrorMemoryAllocation) ? BML_ENOMEM : BML_ECUDA;
+    return fail(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define BML_CUDA(call)                                  \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+// ---------------------------------------------------------------- kernel args
+struct StepArgs {
+    const uint2* src;  // row 0 of the source buffer (ghost rows at negative rows)
+    uint2* dst;        // row 0 of the destination buffer
+    int n;             // torus side
+    int W;             // words per row
+    int pitch;         // words between rows
+    int rows;          // rows in this band
+    int strip_rows;    // rows per warp strip (the last strip also takes the remainder)
+    int nstrips;
+    int ncols;         // warp columns per strip
+    int items;         // nstrips * ncols
+    uint32_t last_mask;
+    int single_band;   // ghost rows are images of this band's own rows
+    uint2* up_halo;    // multi-band: output row r < kHalo also goes to up_halo + r*pitch
+    uint2* down_halo;  // multi-band: row r >= rows-kHalo also goes to down_halo + (r-rows)*pitch
+    unsigned long long* up_flag;    // +1 per warp after publishing to up
+    unsigned long long* down_flag;  // +1 per warp after publishing to down
+    const unsigned long long* top_flag;  // wait before reading ghost rows above
+    const unsigned long long* bot_flag;  // wait before reading ghost rows below
+    unsigned long long expect;
+    unsigned long long* metrics;  // [4][stride]: lr_moved, tb_moved, lr_count, tb_count
+    int metrics_stride;
+    int step_base;
+    int* error_flag;
+};
+
+// --------------------------------------------------------------- device utils
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Spin until *flag >= expect (peer publication of ghost rows). Bounded so a
+// broken peer cannot hang the GPU: after ~4 s the error flag is raised.
+__device__ void wait_flag(const unsigned long long* flag, unsigned long long expect, int* err) {
+    if (threadIdx.x % 32 == 0) {
+        const long long t0 = clock64();
+        while (ld_acquire_sys(flag) < expect) {
+            __nanosleep(256);
+            if (clock64() - t0 > 8000000000LL) {
+                atomicExch(err, 2);
+                break;
+            }
+        }
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void publish(unsigned long long* flag) {
+    __threadfence_system();
+    __syncwarp();
+    if (threadIdx.x % 32 == 0) atomicAdd_system(flag, 1ull);
+}
+
+// 32 cells starting at cell c0 of a row (0 <= c0 < n), wrapping at n.
+// Fast path: an aligned full word. Slow path (row end, n % 32 != 0, tiny n):
+// gather bit runs across words and across the wrap.
+__device__ __noinline__ uint2 gather_window(const uint2* __restrict__ row, int c0, int n) {
+    uint32_t l = 0, t = 0;
+    int got = 0, c = c0;
+    while (got < 32) {
+        const int q = c >> 5, o = c & 31;
+        int take = min(32 - o, n - c);
+        take = min(take, 32 - got);
+        const uint2 w = __ldcg(row + q);
+        const uint32_t m = (take == 32) ? kFull : ((1u << take) - 1u);
+        l |= ((w.x >> o) & m) << got;
+        t |= ((w.y >> o) & m) << got;
+        got += take;
+        c += take;
+        if (c >= n) c = 0;
+    }
+    return make_uint2(l, t);
+}
+
+template <int MODE>
+__device__ __forceinline__ uint2 load_cells(const uint2* row, int word, int c0, int n,
+                                            bool coherent) {
+    if (MODE == kGeneric) {
+        if ((c0 & 31) == 0 && c0 + 32 <= n) return coherent ? __ldcg(row + (c0 >> 5)) : __ldg(row + (c0 >> 5));
+        return gather_window(row, c0, n);
+    }
+    return coherent ? __ldcg(row + word) : __ldg(row + word);
+}
+
+__device__ __forceinline__ void put(uint2* p, uint32_t l, uint32_t t) { *p = make_uint2(l, t); }
+
+// ------------------------------------------------------- temporally blocked step
+//
+// Warp w handles (strip, col). Lane l stands for the 32 cells starting at
+// cell 32*(30*col + l - 1) (mod n): lanes 1..30 are outputs, lanes 0 and 31
+// are ghost words whose outer bits go stale by one cell per step. In
+// kFullRow mode (W == 32) lane l is word l and shuffles wrap exactly.
+//
+// Software pipeline: stage s (step s+1 of the block) at loop index j consumes
+// row j-2s at time s (produced by stage s-1 one iteration earlier, so all K
+// stages of an iteration are independent) and emits row j-2s-1 at time s+1.
+// Stage K-1 therefore emits row j-2K+1 at time K.
+template <int K, int MODE, bool COUNT>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+step_block_kernel(const StepArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int warps_total = gridDim.x * kWarpsPerCta;
+    for (int item = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5); item < a.items;
+         item += warps_total) {
+        const int strip = item / a.ncols;
+        const int col = item - strip * a.ncols;
+        const int r_lo = strip * a.strip_rows;
+        const int r_hi = (strip == a.nstrips - 1) ? a.rows : r_lo + a.strip_rows;
+
+        int word = lane, c0 = 0, out_word = lane;
+        uint32_t valid = kFull;
+        if (MODE != kFullRow) {
+            const int w = col * kOutWords + lane - 1;
+            const bool is_out = lane >= 1 && lane <= kOutWords && w < a.W;
+            out_word = w;
+            valid = is_out ? (w == a.W - 1 ? a.last_mask : kFull) : 0u;
+            word = ((w % a.W) + a.W) % a.W;
+            long long cc = (32LL * w) % a.n;
+            if (cc < 0) cc += a.n;
+            c0 = static_cast<int>(cc);
+        }
+
+        const bool top_strip = r_lo == 0;
+        const bool bot_strip = r_hi == a.rows;
+        if (!a.single_band) {
+            if (top_strip) wait_flag(a.top_flag, a.expect, a.error_flag);
+            if (bot_strip) wait_flag(a.bot_flag, a.expect, a.error_flag);
+        }
+
+        uint32_t pl[K + 1], pt[K + 1];           // stage inputs, one iteration old
+        uint32_t tA[K], tB[K], eB[K], lB[K];     // per-stage TB window
+        uint32_t cm[K], cc[K];                   // packed 16-bit counters
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            pl[s] = pt[s] = tA[s] = tB[s] = eB[s] = lB[s] = 0u;
+            cm[s] = cc[s] = 0u;
+        }
+        pl[K] = pt[K] = 0u;
+
+        const int j_begin = r_lo - K;
+        const int j_load_end = r_hi + K;
+        const int j_end = r_hi + 2 * K - 1;
+        const bool coherent = !a.single_band;
+
+        auto fetch = [&](int j) -> uint2 {
+            if (j >= j_load_end) return make_uint2(0u, 0u);
+            const uint2* row = a.src + static_cast<long long>(j) * a.pitch;
+            return load_cells<MODE>(row, word, c0, a.n, coherent && (j < 0 || j >= a.rows));
+        };
+
+        uint2 nx0 = fetch(j_begin);
+        uint2 nx1 = fetch(j_begin + 1);
+        for (int j = j_begin; j < j_end; ++j) {
+            const uint2 x = nx0;
+            nx0 = nx1;
+            nx1 = fetch(j + 2);
+#pragma unroll
+            for (int s = K - 1; s >= 0; --s) {
+                const uint32_t L = (s == 0) ? x.x : pl[s];
+                const uint32_t T = (s == 0) ? x.y : pt[s];
+                // ---- LR phase on row rho = j - 2s
+                const uint32_t E = ~(L | T);
+                uint32_t Ll, Er;
+                if (MODE == kFullRow) {
+                    Ll = __shfl_sync(kFull, L, (lane + 31) & 31);
+                    Er = __shfl_sync(kFull, E, (lane + 1) & 31);
+                } else {
+                    Ll = __shfl_up_sync(kFull, L, 1);
+                    Er = __shfl_down_sync(kFull, E, 1);
+                }
+                const uint32_t prevL = __funnelshift_l(Ll, L, 1);
+                const uint32_t nextE = __funnelshift_r(E, Er, 1);
+                const uint32_t vac = L & nextE;
+                const uint32_t Lp = (prevL & E) | (L ^ vac);
+                const uint32_t Ep = ~(Lp | T);
+                // ---- TB phase emits row rho - 1
+                const uint32_t vacT = tB[s] & Ep;
+                const uint32_t newT = (tA[s] & eB[s]) | (tB[s] ^ vacT);
+                const uint32_t newL = lB[s];
+                if (COUNT) {
+                    const int rho = j - 2 * s;
+                    if (static_cast<unsigned>(rho - r_lo) < static_cast<unsigned>(r_hi - r_lo))
+                        cm[s] += __popc(vac & valid);
+                    if (static_cast<unsigned>(rho - 1 - r_lo) < static_cast<unsigned>(r_hi - r_lo)) {
+                        cm[s] += static_cast<uint32_t>(__popc(vacT & valid)) << 16;
+                        cc[s] += __popc(newL & valid) +
+                                 (static_cast<uint32_t>(__popc(newT & valid)) << 16);
+                    }
+                }
+                tA[s] = tB[s];
+                tB[s] = T;
+                eB[s] = Ep;
+                lB[s] = Lp;
+                if (s < K - 1) {
+                    pl[s + 1] = newL;
+                    pt[s + 1] = newT;
+                } else {
+                    const int o = j - 2 * K + 1;
+                    if (o >= r_lo) {
+                        const uint32_t ol = newL & valid, ot = newT & valid;
+                        if (valid) {
+                            put(a.dst + static_cast<long long>(o) * a.pitch + out_word, ol, ot);
+                            if (a.single_band) {
+                                for (int h = o - a.n; h >= -kHalo; h -= a.n)
+                                    put(a.dst + static_cast<long long>(h) * a.pitch + out_word, ol, ot);
+                                for (int h = o + a.n; h < a.rows + kHalo; h += a.n)
+                                    put(a.dst + static_cast<long long>(h) * a.pitch + out_word, ol, ot);
+                            } else {
+                                if (o < kHalo)
+                                    put(a.up_halo + static_cast<long long>(o) * a.pitch + out_word, ol, ot);
+                                if (o >= a.rows - kHalo)
+                                    put(a.down_halo + static_cast<long long>(o - a.rows) * a.pitch + out_word, ol, ot);
+                            }
+                        }
+                        if (!a.single_band) {
+                            if (o == kHalo - 1) publish(a.up_flag);
+                            if (o == a.rows - 1) publish(a.down_flag);
+                        }
+                    }
+                }
+            }
+        }
+
+        if (COUNT) {
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                const unsigned v0 = __reduce_add_sync(kFull, cm[s] & 0xffffu);
+                const unsigned v1 = __reduce_add_sync(kFull, cm[s] >> 16);
+                const unsigned v2 = __reduce_add_sync(kFull, cc[s] & 0xffffu);
+                const unsigned v3 = __reduce_add_sync(kFull, cc[s] >> 16);
+                if (lane == 0) {
+                    unsigned long long* m = a.metrics + a.step_base + s;
+                    if (v0) atomicAdd(m, static_cast<unsigned long long>(v0));
+                    if (v1) atomicAdd(m + a.metrics_stride, static_cast<unsigned long long>(v1));
+                    if (v2) atomicAdd(m + 2 * a.metrics_stride, static_cast<unsigned long long>(v2));
+                    if (v3) atomicAdd(m + 3 * a.metrics_stride, static_cast<unsigned long long>(v3));
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ single phases
+// One thread per (row, word) of the band; used by step_phase (bml_dev_phase).
+struct PhaseArgs {
+    const uint2* src;
+    uint2* dst;
+    int n, W, pitch, rows;
+    uint32_t last_mask;
+    unsigned long long* moved;
+};
+
+__device__ __forceinline__ void put_with_images(const PhaseArgs& a, int r, int w, uint32_t l,
+                                                uint32_t t) {
+    put(a.dst + static_cast<long long>(r) * a.pitch + w, l, t);
+    for (int h = r - a.n; h >= -kHalo; h -= a.n) put(a.dst + static_cast<long long>(h) * a.pitch + w, l, t);
+    for (int h = r + a.n; h < a.rows + kHalo; h += a.n) put(a.dst + static_cast<long long>(h) * a.pitch + w, l, t);
+}
+
+__global__ void phase_h_kernel(const PhaseArgs a) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool live = idx < static_cast<long long>(a.rows) * a.W;
+    uint32_t moved = 0;
+    if (live) {
+        const int r = static_cast<int>(idx / a.W), w = static_cast<int>(idx % a.W);
+        const uint2* row = a.src + static_cast<long long>(r) * a.pitch;
+        const int c = 32 * w;
+        const uint2 x = gather_window(row, c, a.n);
+        const uint2 left = gather_window(row, ((c - 32) % a.n + a.n) % a.n, a.n);
+        const uint2 right = gather_window(row, (c + 32) % a.n, a.n);
+        const uint32_t E = ~(x.x | x.y);
+        const uint32_t Er = ~(right.x | right.y);
+        const uint32_t prevL = __funnelshift_l(left.x, x.x, 1);
+        const uint32_t nextE = __funnelshift_r(E, Er, 1);
+        const uint32_t valid = (w == a.W - 1) ? a.last_mask : kFull;
+        const uint32_t vac = x.x & nextE & valid;
+        const uint32_t Lp = ((prevL & E) | (x.x & ~nextE)) & valid;
+        moved = __popc(vac);
+        put_with_images(a, r, w, Lp, x.y & valid);
+    }
+    moved = __reduce_add_sync(kFull, moved);
+    if ((threadIdx.x & 31) == 0 && moved) atomicAdd(a.moved, static_cast<unsigned long long>(moved));
+}
+
+__global__ void phase_v_kernel(const PhaseArgs a) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool live = idx < static_cast<long long>(a.rows) * a.W;
+    uint32_t moved = 0;
+    if (live) {
+        const int r = static_cast<int>(idx / a.W), w = static_cast<int>(idx % a.W);
+        const uint2 up = a.src[static_cast<long long>(r - 1) * a.pitch + w];
+        const uint2 x = a.src[static_cast<long long>(r) * a.pitch + w];
+        const uint2 dn = a.src[static_cast<long long>(r + 1) * a.pitch + w];
+        const uint32_t E = ~(x.x | x.y);
+        const uint32_t Ed = ~(dn.x | dn.y);
+        const uint32_t valid = (w == a.W - 1) ? a.last_mask : kFull;
+        const uint32_t vac = x.y & Ed & valid;
+        const uint32_t Tp = ((up.y & E) | (x.y & ~Ed)) & valid;
+        moved = __popc(vac);
+        put_with_images(a, r, w, x.x & valid, Tp);
+    }
+    moved = __reduce_add_sync(kFull, moved);
+    if ((threadIdx.x & 31) == 0 && moved) atomicAdd(a.moved, static_cast<unsigned long long>(moved));
+}
+
+// ------------------------------------------------------------ pack / unpack
+// Byte lattice (0/1/2 per cell, `bpitch` bytes per row) <-> bit planes.
+__device__ __forceinline__ uint32_t gather4(uint32_t x) {  // bit 0 of 4 bytes -> 4 bits
+    return ((x & 0x01010101u) * 0x01020408u) >> 24;
+}
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) {  // 4 bits -> bit 0 of 4 bytes
+    return (nib * 0x00204081u) & 0x01010101u;
+}
+
+__global__ void pack_kernel(const uint8_t* __restrict__ bytes, long long bpitch, uint2* dst,
+                            int n, int W, int pitch, int rows, int* bad) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long long>(rows) * W) return;
+    const int r = static_cast<int>(idx / W), w = static_cast<int>(idx % W);
+    const uint8_t* p = bytes + r * bpitch + 32LL * w;
+    const int cells = min(32, n - 32 * w);
+    uint32_t l = 0, t = 0, badbits = 0;
+    if (cells == 32 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+        const uint4 v0 = *reinterpret_cast<const uint4*>(p);
+        const uint4 v1 = *reinterpret_cast<const uint4*>(p + 16);
+        const uint32_t v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            l |= gather4(v[i]) << (4 * i);
+            t |= gather4(v[i] >> 1) << (4 * i);
+            badbits |= (v[i] & 0xfcfcfcfcu) | (v[i] & (v[i] >> 1) & 0x01010101u);
+        }
+    } else {
+        for (int i = 0; i < cells; ++i) {
+            const uint32_t b = p[i];
+            l |= (b & 1u) << i;
+            t |= ((b >> 1) & 1u) << i;
+            badbits |= (b > 2u);
+        }
+    }
+    if (badbits) atomicExch(bad, 1);
+    dst[static_cast<long long>(r) * pitch + w] = make_uint2(l, t);
+}
+
+__global__ void unpack_kernel(const uint2* __restrict__ src, uint8_t* bytes, long long bpitch,
+                              int n, int W, int pitch, int rows) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long long>(rows) * W) return;
+    const int r = static_cast<int>(idx / W), w = static_cast<int>(idx % W);
+    const uint2 x = src[static_cast<long long>(r) * pitch + w];
+    uint8_t* p = bytes + r * bpitch + 32LL * w;
+    const int cells = min(32, n - 32 * w);
+    if (cells == 32 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+        uint32_t v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            v[i] = spread4((x.x >> (4 * i)) & 15u) | (spread4((x.y >> (4 * i)) & 15u) << 1);
+        *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<uint4*>(p + 16) = make_uint4(v[4], v[5], v[6], v[7]);
+    } else {
+        for (int i = 0; i < cells; ++i)
+            p[i] = static_cast<uint8_t>(((x.x >> i) & 1u) | (((x.y >> i) & 1u) << 1));
+    }
+}
+
+// Ghost rows of a single band: row h in [-kHalo,0) U [rows, rows+kHalo) is
+// the image of row (h mod n).
+__global__ void fill_images_kernel(uint2* buf, int n, int W, int pitch, int rows) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= 2 * kHalo * W) return;
+    const int g = idx / W, w = idx % W;
+    const int h = g < kHalo ? g - kHalo : rows + (g - kHalo);
+    const int src = ((h % n) + n) % n;
+    buf[static_cast<long long>(h) * pitch + w] = buf[static_cast<long long>(src) * pitch + w];
+}
+
+// Multi-band: publish the band's first/last kHalo rows into the neighbours'
+// ghost rows of the same parity and raise their flags (one signal per warp
+// column, matching the step kernel's accounting).
+__global__ void push_halo_kernel(const uint2* buf, int W, int pitch, int rows, uint2* up_halo,
+                                 uint2* down_halo, unsigned long long* up_flag,
+                                 unsigned long long* down_flag, int ncols) {
+    for (int idx = threadIdx.x; idx < kHalo * W; idx += blockDim.x) {
+        const int r = idx / W, w = idx % W;
+        up_halo[static_cast<long long>(r) * pitch + w] = buf[static_cast<long long>(r) * pitch + w];
+        const int rb = rows - kHalo + r;
+        down_halo[static_cast<long long>(rb - rows) * pitch + w] =
+            buf[static_cast<long long>(rb) * pitch + w];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd_system(up_flag, static_cast<unsigned long long>(ncols));
+        atomicAdd_system(down_flag, static_cast<unsigned long long>(ncols));
+    }
+}
+
+__global__ void counts_kernel(const uint2* __restrict__ buf, int W, int pitch, int rows,
+                              unsigned long long* out) {
+    unsigned long long lr = 0, tb = 0;
+    const long long total = static_cast<long long>(rows) * W;
+    for (long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(idx / W), w = static_cast<int>(idx % W);
+        const uint2 x = buf[static_cast<long long>(r) * pitch + w];
+        lr += __popc(x.x);
+        tb += __popc(x.y);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lr += __shfl_xor_sync(kFull, lr, o);
+        tb += __shfl_xor_sync(kFull, tb, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (lr) atomicAdd(out, lr);
+        if (tb) atomicAdd(out + 1, tb);
+    }
+}
+
+// ------------------------------------------------------------ dispatch table
+using StepKernel = void (*)(const StepArgs);
+
+template <int MODE, bool COUNT>
+StepKernel pick_k(int k) {
+    switch (k) {
+        case 1: return step_block_kernel<1, MODE, COUNT>;
+        case 2: return step_block_kernel<2, MODE, COUNT>;
+        case 4: return step_block_kernel<4, MODE, COUNT>;
+        case 8: return step_block_kernel<8, MODE, COUNT>;
+        case 16: return step_block_kernel<16, MODE, COUNT>;
+        default: return nullptr;
+    }
+}
+
+StepKernel pick(int k, int mode, bool count) {
+    if (mode == kFullRow) return count ? pick_k<kFullRow, true>(k) : pick_k<kFullRow, false>(k);
+    if (mode == kAligned) return count ? pick_k<kAligned, true>(k) : pick_k<kAligned, false>(k);
+    return count ? pick_k<kGeneric, true>(k) : pick_k<kGeneric, false>(k);
+}
+
+int largest_block_at_most(long long remaining, int cap) {
+    int k = 16;
+    while (k > 1 && (k > remaining || k > cap)) k >>= 1;
+    return k;
+}
+
+struct IpcBlob {
+    uint32_t magic;
+    int32_t n, row_begin, row_end, pitch, W;
+    int32_t pid;
+    int32_t device;
+    cudaIpcMemHandle_t buf[2];
+    cudaIpcMemHandle_t flags;
+};
+static_assert(sizeof(IpcBlob) <= BML_EXPORT_BYTES, "blob too large");
+constexpr uint32_t kBlobMagic = 0xB200B31Eu;
+
+}  // namespace
+
+// ================================================================ handle
+struct bml_dev {
+    int n = 0, W = 0, pitch = 0;
+    int row_begin = 0, row_end = 0, rows = 0;
+    int device = 0;
+    uint32_t last_mask = kFull;
+    int mode = kGeneric;
+    int block_steps = 8;
+    int strip_rows = 256;
+    int sms = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    uint2* buf[2] = {nullptr, nullptr};  // allocation bases
+    int cur = 0;
+    uint8_t* staging = nullptr;          // rows * n bytes
+    unsigned long long* scratch = nullptr;  // 4 words: counts / moved
+    int* err = nullptr;                  // [0]: bad upload cell, [1]: flag timeout
+    unsigned long long* flags = nullptr;  // [0]: top (from up), [1]: bottom (from down)
+    unsigned long long* metrics = nullptr;
+    long long metrics_cap = 0;
+    // multi-band links
+    bool connected = false;
+    uint2* up_halo[2] = {nullptr, nullptr};
+    uint2* down_halo[2] = {nullptr, nullptr};
+    unsigned long long* up_flag = nullptr;    // neighbour above: its bottom flag
+    unsigned long long* down_flag = nullptr;  // neighbour below: its top flag
+    std::vector<void*> ipc_opened;
+    unsigned long long pubs = 0;
+    // timing
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    long long launches = 0;
+    double kernel_ms = 0.0;
+
+    uint2* row0(int parity) const { return buf[parity] + static_cast<long long>(kHalo) * pitch; }
+    bool single_band() const { return rows == n && row_begin == 0; }
+    int ncols() const { return mode == kFullRow ? 1 : (W + kOutWords - 1) / kOutWords; }
+};
+
+namespace {
+
+int check(bml_dev* d) {
+    if (!d) return fail(BML_EINVAL, "null bml_dev handle");
+    cudaError_t e = cudaSetDevice(d->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    return BML_OK;
+}
+
+cudaEvent_t take_event(bml_dev* d) {
+    if (!d->ev_pool.empty()) {
+        cudaEvent_t e = d->ev_pool.back();
+        d->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void harvest_timing(bml_dev* d) {
+    for (auto& pr : d->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) d->kernel_ms += ms;
+        d->ev_pool.push_back(pr.first);
+        d->ev_pool.push_back(pr.second);
+    }
+    d->pending.clear();
+}
+
+int ensure_metrics(bml_dev* d, long long steps) {
+    const long long need = 4 * steps;
+    if (need <= d->metrics_cap) return BML_OK;
+    if (d->metrics) cudaFree(d->metrics);
+    d->metrics = nullptr;
+    d->metrics_cap = 0;
+    BML_CUDA(cudaMalloc(&d->metrics, need * sizeof(unsigned long long)));
+    d->metrics_cap = need;
+    return BML_OK;
+}
+
+int fill_images(bml_dev* d, int parity) {
+    const int total = 2 * kHalo * d->W;
+    fill_images_kernel<<<(total + 255) / 256, 256, 0, d->stream>>>(d->row0(parity), d->n, d->W,
+                                                                   d->pitch, d->rows);
+    BML_CUDA(cudaGetLastError());
+    return BML_OK;
+}
+
+int create_common(int n, int row_begin, int row_end, int device, bml_dev** out) {
+    if (!out) return fail(BML_EINVAL, "bml_dev_create: out is null");
+    *out = nullptr;
+    if (n < 1) return fail(BML_EINVAL, "bml_dev_create: n must be >= 1");
+    if (row_begin < 0 || row_end > n || row_begin >= row_end)
+        return fail(BML_EINVAL, "bml_dev_create_band: need 0 <= row_begin < row_end <= n");
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (device < 0) {
+        e = cudaGetDevice(&device);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    }
+    if (device < 0 || device >= count)
+        return fail(BML_EINVAL, "bml_dev_create: device " + std::to_string(device) + " out of range");
+    e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+
+    bml_dev* d = new (std::nothrow) bml_dev;
+    if (!d) return fail(BML_ENOMEM, "host allocation failed");
+    d->n = n;
+    d->W = (n + 31) / 32;
+    d->pitch = (d->W + 15) / 16 * 16;  // 128-byte aligned rows
+    d->row_begin = row_begin;
+    d->row_end = row_end;
+    d->rows = row_end - row_begin;
+    d->device = device;
+    const int nb = n - 32 * (d->W - 1);
+    d->last_mask = nb == 32 ? kFull : ((1u << nb) - 1u);
+    d->mode = (n % 32 != 0) ? kGeneric : (d->W == 32 ? kFullRow : kAligned);
+    cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, device);
+    if (d->single_band() && n <= 2048) d->strip_rows = std::max(16, n / 64);
+
+    auto bail = [&](cudaError_t err, const char* what) {
+        bml_dev_destroy(d);
+        return cuda_fail(err, what);
+    };
+    const size_t words = static_cast<size_t>(d->rows + 2 * kHalo) * d->pitch;
+    for (int p = 0; p < 2; ++p) {
+        if ((e = cudaMalloc(&d->buf[p], words * sizeof(uint2))) != cudaSuccess)
+            return bail(e, "cudaMalloc(lattice)");
+        if ((e = cudaMemset(d->buf[p], 0, words * sizeof(uint2))) != cudaSuccess)
+            return bail(e, "cudaMemset(lattice)");
+    }
+    if ((e = cudaMalloc(&d->staging, static_cast<size_t>(d->rows) * n)) != cudaSuccess)
+        return bail(e, "cudaMalloc(staging)");
+    if ((e = cudaMalloc(&d->scratch, 4 * sizeof(unsigned long long))) != cudaSuccess)
+        return bail(e, "cudaMalloc(scratch)");
+    if ((e = cudaMalloc(&d->err, 4 * sizeof(int))) != cudaSuccess) return bail(e, "cudaMalloc(err)");
+    if ((e = cudaMemset(d->err, 0, 4 * sizeof(int))) != cudaSuccess) return bail(e, "cudaMemset(err)");
+    if ((e = cudaMalloc(&d->flags, 2 * sizeof(unsigned long long))) != cudaSuccess)
+        return bail(e, "cudaMalloc(flags)");
+    if ((e = cudaMemset(d->flags, 0, 2 * sizeof(unsigned long long))) != cudaSuccess)
+        return bail(e, "cudaMemset(flags)");
+    if ((e = cudaStreamCreateWithFlags(&d->own_stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return bail(e, "cudaStreamCreate");
+    d->stream = d->own_stream;
+    *out = d;
+    return BML_OK;
+}
+
+int check_errors(bml_dev* d) {
+    int h[4] = {0, 0, 0, 0};
+    cudaError_t e = cudaMemcpyAsync(h, d->err, sizeof h, cudaMemcpyDeviceToHost, d->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "error-flag readback");
+    if (h[1]) {
+        cudaMemsetAsync(d->err, 0, 4 * sizeof(int), d->stream);
+        return fail(BML_ECUDA, "halo flag wait timed out (neighbour band stalled)");
+    }
+    return BML_OK;
+}
+
+int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_stride) {
+    StepKernel kern = pick(k, d->mode, count);
+    if (!kern) return fail(BML_EINVAL, "unsupported block depth " + std::to_string(k));
+    const int strip = d->strip_rows;
+    // floor: every strip has >= strip_rows rows (the last absorbs the
+    // remainder), so the ghost-row sources of a band never straddle strips
+    const int nstrips = std::max(1, d->rows / strip);
+    StepArgs a{};
+    a.src = d->row0(d->cur);
+    a.dst = d->row0(d->cur ^ 1);
+    a.n = d->n;
+    a.W = d->W;
+    a.pitch = d->pitch;
+    a.rows = d->rows;
+    a.strip_rows = strip;
+    a.nstrips = nstrips;
+    a.ncols = d->ncols();
+    a.items = nstrips * a.ncols;
+    a.last_mask = d->last_mask;
+    a.single_band = d->connected ? 0 : 1;
+    const int nxt = d->cur ^ 1;
+    a.up_halo = d->up_halo[nxt];
+    a.down_halo = d->down_halo[nxt];
+    a.up_flag = d->up_flag;
+    a.down_flag = d->down_flag;
+    a.top_flag = d->flags;
+    a.bot_flag = d->flags + 1;
+    a.expect = d->pubs * static_cast<unsigned long long>(a.ncols);
+    a.metrics = d->metrics;
+    a.metrics_stride = metrics_stride;
+    a.step_base = step_base;
+    a.error_flag = d->err + 1;
+
+    int max_ctas_per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_ctas_per_sm, kern, kWarpsPerCta * 32, 0);
+    max_ctas_per_sm = std::max(1, max_ctas_per_sm);
+    const int want = (a.items + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int grid = std::max(1, std::min(want, d->sms * max_ctas_per_sm));
+
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (d->timing) {
+        e0 = take_event(d);
+        e1 = take_event(d);
+        cudaEventRecord(e0, d->stream);
+    }
+    kern<<<grid, kWarpsPerCta * 32, 0, d->stream>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "step_block_kernel launch");
+    if (d->timing) {
+        cudaEventRecord(e1, d->stream);
+        d->pending.emplace_back(e0, e1);
+    }
+    ++d->launches;
+    d->cur ^= 1;
+    if (d->connected) ++d->pubs;
+    return BML_OK;
+}
+
+}  // namespace
+
+// ================================================================ C-ABI
+extern "C" {
+
+const char* bml_dev_last_error(void) { return g_last_error.c_str(); }
+
+const char* bml_dev_version(void) { return "bml_dev 0.1.0 sm_100a bitplane-temporal"; }
+
+int bml_dev_device_count(int* count) {
+    if (!count) return fail(BML_EINVAL, "bml_dev_device_count: null pointer");
+    *count = 0;
+    cudaError_t e = cudaGetDeviceCount(count);
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+        (void)cudaGetLastError();
+        *count = 0;
+        return BML_OK;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    return BML_OK;
+}
+
+int bml_dev_create(int n, int device, bml_dev** out) {
+    return create_common(n, 0, n, device, out);
+}
+
+int bml_dev_create_band(int n, int row_begin, int row_end, int device, bml_dev** out) {
+    if (row_end - row_begin < kHalo && !(row_begin == 0 && row_end == n))
+        return fail(BML_EINVAL, "bml_dev_create_band: a band needs >= 16 rows");
+    return create_common(n, row_begin, row_end, device, out);
+}
+
+int bml_dev_destroy(bml_dev* d) {
+    if (!d) return BML_OK;
+    cudaSetDevice(d->device);
+    if (d->stream) cudaStreamSynchronize(d->stream);
+    for (void* p : d->ipc_opened) cudaIpcCloseMemHandle(p);
+    for (int p = 0; p < 2; ++p) cudaFree(d->buf[p]);
+    cudaFree(d->staging);
+    cudaFree(d->scratch);
+    cudaFree(d->err);
+    cudaFree(d->flags);
+    cudaFree(d->metrics);
+    for (auto& pr : d->pending) {
+        d->ev_pool.push_back(pr.first);
+        d->ev_pool.push_back(pr.second);
+    }
+    for (cudaEvent_t e : d->ev_pool) cudaEventDestroy(e);
+    if (d->own_stream) cudaStreamDestroy(d->own_stream);
+    delete d;
+    return BML_OK;
+}
+
+int bml_dev_set_stream(bml_dev* d, void* stream) {
+    if (int rc = check(d)) return rc;
+    d->stream = stream ? static_cast<cudaStream_t>(stream) : d->own_stream;
+    return BML_OK;
+}
+
+int bml_dev_sync(bml_dev* d) {
+    if (int rc = check(d)) return rc;
+    BML_CUDA(cudaStreamSynchronize(d->stream));
+    return check_errors(d);
+}
+
+int bml_dev_configure(bml_dev* d, int block_steps, int strip_rows) {
+    if (int rc = check(d)) return rc;
+    if (block_steps) {
+        if (block_steps != 1 && block_steps != 2 && block_steps != 4 && block_steps != 8 &&
+            block_steps != 16)
+            return fail(BML_EINVAL, "block_steps must be one of 1, 2, 4, 8, 16");
+        d->block_steps = block_steps;
+    }
+    if (strip_rows) {
+        if (strip_rows < 1 || strip_rows > 1000)
+            return fail(BML_EINVAL, "strip_rows must be in [1, 1000]");
+        if (d->connected && strip_rows < kHalo)
+            return fail(BML_EINVAL, "connected bands need strip_rows >= 16");
+        d->strip_rows = strip_rows;
+    }
+    return BML_OK;
+}
+
+int bml_dev_info(bml_dev* d, int* n, int* row_begin, int* row_end, int* block_steps,
+                 int* strip_rows, size_t* device_bytes) {
+    if (!d) return fail(BML_EINVAL, "null bml_dev handle");
+    if (n) *n = d->n;
+    if (row_begin) *row_begin = d->row_begin;
+    if (row_end) *row_end = d->row_end;
+    if (block_steps) *block_steps = d->block_steps;
+    if (strip_rows) *strip_rows = d->strip_rows;
+    if (device_bytes)
+        *device_bytes = 2 * static_cast<size_t>(d->rows + 2 * kHalo) * d->pitch * sizeof(uint2) +
+                        static_cast<size_t>(d->rows) * d->n;
+    return BML_OK;
+}
+
+int bml_dev_enable_timing(bml_dev* d, int enable) {
+    if (int rc = check(d)) return rc;
+    d->timing = enable != 0;
+    return BML_OK;
+}
+
+int bml_dev_kernel_stats(bml_dev* d, int64_t* launches, double* kernel_ms, int reset) {
+    if (int rc = check(d)) return rc;
+    BML_CUDA(cudaStreamSynchronize(d->stream));
+    harvest_timing(d);
+    if (launches) *launches = d->launches;
+    if (kernel_ms) *kernel_ms = d->kernel_ms;
+    if (reset) {
+        d->launches = 0;
+        d->kernel_ms = 0.0;
+    }
+    return BML_OK;
+}
+
+int bml_dev_upload(bml_dev* d, const uint8_t* src, size_t src_pitch) {
+    if (int rc = check(d)) return rc;
+    if (!src) return fail(BML_EINVAL, "bml_dev_upload: src is null");
+    if (src_pitch < static_cast<size_t>(d->n))
+        return fail(BML_EINVAL, "bml_dev_upload: pitch smaller than a row");
+    BML_CUDA(cudaMemsetAsync(d->err, 0, 4 * sizeof(int), d->stream));
+    BML_CUDA(cudaMemcpy2DAsync(d->staging, d->n, src, src_pitch, d->n, d->rows,
+                               cudaMemcpyDefault, d->stream));
+    const long long total = static_cast<long long>(d->rows) * d->W;
+    pack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, d->stream>>>(
+        d->staging, d->n, d->row0(d->cur), d->n, d->W, d->pitch, d->rows, d->err);
+    BML_CUDA(cudaGetLastError());
+    if (d->single_band()) {
+        if (int rc = fill_images(d, d->cur)) return rc;
+    }
+    int bad = 0;
+    BML_CUDA(cudaMemcpyAsync(&bad, d->err, sizeof(int), cudaMemcpyDeviceToHost, d->stream));
+    BML_CUDA(cudaStreamSynchronize(d->stream));
+    if (bad) return fail(BML_EINVAL, "bml_dev_upload: cell value outside {0,1,2}");
+    return BML_OK;
+}
+
+int bml_dev_download(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
+    if (int rc = check(d)) return rc;
+    if (!dst) return fail(BML_EINVAL, "bml_dev_download: dst is null");
+    if (dst_pitch < static_cast<size_t>(d->n))
+        return fail(BML_EINVAL, "bml_dev_download: pitch smaller than a row");
+    const long long total = static_cast<long long>(d->rows) * d->W;
+    unpack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, d->stream>>>(
+        d->row0(d->cur), d->staging, d->n, d->n, d->W, d->pitch, d->rows);
+    BML_CUDA(cudaGetLastError());
+    BML_CUDA(cudaMemcpy2DAsync(dst, dst_pitch, d->staging, d->n, d->n, d->rows,
+                               cudaMemcpyDefault, d->stream));
+    BML_CUDA(cudaStreamSynchronize(d->stream));
+    return check_errors(d);
+}
+
+int bml_dev_init_random(bml_dev* d, double rho, uint64_t seed) {
+    (void)rho;
+    (void)seed;
+    if (int rc = check(d)) return rc;
+    return fail(BML_EINVAL, "bml_dev_init_random: device-side init_grid not available in this build");
+}
+
+int bml_dev_counts(bml_dev* d, int64_t* lr, int64_t* tb) {
+    if (int rc = check(d)) return rc;
+    BML_CUDA(cudaMemsetAsync(d->scratch, 0, 2 * sizeof(unsigned long long), d->stream));
+    counts_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->row0(d->cur), d->W, d->pitch, d->rows,
+                                                     d->scratch);
+    BML_CUDA(cudaGetLastError());
+    unsigned long long h[2];
+    BML_CUDA(cudaMemcpyAsync(h, d->scratch, sizeof h, cudaMemcpyDeviceToHost, d->stream));
+    BML_CUDA(cudaStreamSynchronize(d->stream));
+    if (lr) *lr = static_cast<int64_t>(h[0]);
+    if (tb) *tb = static_cast<int64_t>(h[1]);
+    return BML_OK;
+}
+
+int bml_dev_phase(bml_dev* d, int phase, int64_t* moved) {
+    if (int rc = check(d)) return rc;
+    if (phase != BML_PHASE_HORIZONTAL && phase != BML_PHASE_VERTICAL)
+        return fail(BML_EINVAL, "bml_dev_phase: phase must be 0 (horizontal) or 1 (vertical)");
+    if (!d->single_band())
+        return fail(BML_EINVAL, "bml_dev_phase: single phases need a single-band handle");
+    BML_CUDA(cudaMemsetAsync(d->scratch, 0, sizeof(unsigned long long), d->stream));
+    PhaseArgs a{};
+    a.src = d->row0(d->cur);
+    a.dst = d->row0(d->cur ^ 1);
+    a.n = d->n;
+    a.W = d->W;
+    a.pitch = d->pitch;
+    a.rows = d->rows;
+    a.last_mask = d->last_mask;
+    a.moved = d->scratch;
+    const long long total = static_cast<long long>(d->rows) * d->W;
+    const unsigned grid = static_cast<unsigned>((total + 255) / 256);
+    if (phase == BML_PHASE_HORIZONTAL)
+        phase_h_kernel<<<grid, 256, 0, d->stream>>>(a);
+    else
+        phase_v_kernel<<<grid, 256, 0, d->stream>>>(a);
+    BML_CUDA(cudaGetLastError());
+    d->cur ^= 1;
+    if (moved) {
+        unsigned long long h = 0;
+        BML_CUDA(cudaMemcpyAsync(&h, d->scratch, sizeof h, cudaMemcpyDeviceToHost, d->stream));
+        BML_CUDA(cudaStreamSynchronize(d->stream));
+        *moved = static_cast<int64_t>(h);
+    }
+    return BML_OK;
+}
+
+int bml_dev_step(bml_dev* d, int64_t steps, int64_t* lr_moved, int64_t* tb_moved,
+                 int64_t* lr_count, int64_t* tb_count) {
+    if (int rc = check(d)) return rc;
+    if (steps < 0) return fail(BML_EINVAL, "bml_dev_step: steps must be >= 0");
+    if (steps == 0) return BML_OK;
+    const bool count = lr_moved || tb_moved || lr_count || tb_count;
+    if (count && steps > (1LL << 26))
+        return fail(BML_EINVAL, "bml_dev_step: at most 2^26 steps per call with metrics");
+    int64_t lr0 = 0, tb0 = 0;
+    const bool check_conservation = (lr_count || tb_count) && d->single_band();
+    if (check_conservation) {
+        if (int rc = bml_dev_counts(d, &lr0, &tb0)) return rc;
+    }
+    if (count) {
+        if (int rc = ensure_metrics(d, steps)) return rc;
+        BML_CUDA(cudaMemsetAsync(d->metrics, 0, 4 * steps * sizeof(unsigned long long), d->stream));
+    }
+    long long done = 0;
+    while (done < steps) {
+        const int k = largest_block_at_most(steps - done, d->block_steps);
+        if (int rc = launch_block(d, k, count, static_cast<int>(done), static_cast<int>(steps)))
+            return rc;
+        done += k;
+    }
+    if (count) {
+        std::vector<unsigned long long> h(static_cast<size_t>(4 * steps));
+        BML_CUDA(cudaMemcpyAsync(h.data(), d->metrics, h.size() * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, d->stream));
+        BML_CUDA(cudaStreamSynchronize(d->stream));
+        for (int64_t s = 0; s < steps; ++s) {
+            if (lr_moved) lr_moved[s] = static_cast<int64_t>(h[s]);
+            if (tb_moved) tb_moved[s] = static_cast<int64_t>(h[steps + s]);
+            if (lr_count) lr_count[s] = static_cast<int64_t>(h[2 * steps + s]);
+            if (tb_count) tb_count[s] = static_cast<int64_t>(h[3 * steps + s]);
+        }
+        if (check_conservation) {
+            for (int64_t s = 0; s < steps; ++s) {
+                if (static_cast<int64_t>(h[2 * steps + s]) != lr0 ||
+                    static_cast<int64_t>(h[3 * steps + s]) != tb0) {
+                    return fail(BML_ECONSERVE,
+                                "conservation violated at step " + std::to_string(s + 1) +
+                                    ": lr " + std::to_string(h[2 * steps + s]) + "/" +
+                                    std::to_string(lr0) + ", tb " +
+                                    std::to_string(h[3 * steps + s]) + "/" + std::to_string(tb0));
+                }
+            }
+        }
+        if (d->connected) return check_errors(d);
+    }
+    return BML_OK;
+}
+
+// ---------------------------------------------------------------- multi-band
+int bml_dev_export(bml_dev* d, void* blob, size_t* size) {
+    if (int rc = check(d)) return rc;
+    if (!blob || !size || *size < sizeof(IpcBlob))
+        return fail(BML_EINVAL, "bml_dev_export: blob buffer too small");
+    IpcBlob b{};
+    b.magic = kBlobMagic;
+    b.n = d->n;
+    b.row_begin = d->row_begin;
+    b.row_end = d->row_end;
+    b.pitch = d->pitch;
+    b.W = d->W;
+    b.device = d->device;
+    for (int p = 0; p < 2; ++p) BML_CUDA(cudaIpcGetMemHandle(&b.buf[p], d->buf[p]));
+    BML_CUDA(cudaIpcGetMemHandle(&b.flags, d->flags));
+    std::memcpy(blob, &b, sizeof b);
+    *size = sizeof b;
+    return BML_OK;
+}
+
+namespace {
+
+int link_peer(bml_dev* d, uint2* const peer_buf[2], unsigned long long* peer_flags, int peer_rows,
+              bool is_up) {
+    for (int p = 0; p < 2; ++p) {
+        uint2* peer_row0 = peer_buf[p] + static_cast<long long>(kHalo) * d->pitch;
+        if (is_up)
+            d->up_halo[p] = peer_row0 + static_cast<long long>(peer_rows) * d->pitch;  // its bottom ghosts
+        else
+            d->down_halo[p] = peer_row0;  // row (r - rows) in [-kHalo, 0): its top ghosts
+    }
+    if (is_up)
+        d->up_flag = peer_flags + 1;  // the neighbour above waits on its bottom flag
+    else
+        d->down_flag = peer_flags;  // the neighbour below waits on its top flag
+    return BML_OK;
+}
+
+int validate_neighbours(bml_dev* d, int up_end, int up_n, int up_pitch, int dn_begin, int dn_n,
+                        int dn_pitch) {
+    if (up_n != d->n || dn_n != d->n || up_pitch != d->pitch || dn_pitch != d->pitch)
+        return fail(BML_EINVAL, "bml_dev_connect: neighbour lattice geometry differs");
+    if (up_end % d->n != d->row_begin)
+        return fail(BML_EINVAL, "bml_dev_connect: up neighbour does not end where this band begins");
+    if (dn_begin != d->row_end % d->n)
+        return fail(BML_EINVAL, "bml_dev_connect: down neighbour does not begin where this band ends");
+    if (d->strip_rows < kHalo) d->strip_rows = kHalo;
+    return BML_OK;
+}
+
+}  // namespace
+
+int bml_dev_connect(bml_dev* d, const void* up_blob, const void* down_blob) {
+    if (int rc = check(d)) return rc;
+    if (!up_blob || !down_blob) return fail(BML_EINVAL, "bml_dev_connect: null blob");
+    IpcBlob up, dn;
+    std::memcpy(&up, up_blob, sizeof up);
+    std::memcpy(&dn, down_blob, sizeof dn);
+    if (up.magic != kBlobMagic || dn.magic != kBlobMagic)
+        return fail(BML_EINVAL, "bml_dev_connect: not a bml_dev export blob");
+    if (int rc = validate_neighbours(d, up.row_end, up.n, up.pitch, dn.row_begin, dn.n, dn.pitch))
+        return rc;
+    const bool same = std::memcmp(&up.buf[0], &dn.buf[0], sizeof(cudaIpcMemHandle_t)) == 0;
+    auto open = [&](const cudaIpcMemHandle_t& h, void** p) -> int {
+        cudaError_t e = cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+        d->ipc_opened.push_back(*p);
+        return BML_OK;
+    };
+    void *ub[2], *uf, *db[2], *df;
+    for (int p = 0; p < 2; ++p)
+        if (int rc = open(up.buf[p], &ub[p])) return rc;
+    if (int rc = open(up.flags, &uf)) return rc;
+    if (same) {
+        db[0] = ub[0];
+        db[1] = ub[1];
+        df = uf;
+    } else {
+        for (int p = 0; p < 2; ++p)
+            if (int rc = open(dn.buf[p], &db[p])) return rc;
+        if (int rc = open(dn.flags, &df)) return rc;
+    }
+    uint2* ubp[2] = {static_cast<uint2*>(ub[0]), static_cast<uint2*>(ub[1])};
+    uint2* dbp[2] = {static_cast<uint2*>(db[0]), static_cast<uint2*>(db[1])};
+    link_peer(d, ubp, static_cast<unsigned long long*>(uf), up.row_end - up.row_begin, true);
+    link_peer(d, dbp, static_cast<unsigned long long*>(df), dn.row_end - dn.row_begin, false);
+    d->connected = true;
+    return BML_OK;
+}
+
+int bml_dev_connect_local(bml_dev* d, bml_dev* up, bml_dev* down) {
+    if (int rc = check(d)) return rc;
+    if (!up || !down) return fail(BML_EINVAL, "bml_dev_connect_local: null neighbour");
+    if (int rc = validate_neighbours(d, up->row_end, up->n, up->pitch, down->row_begin, down->n,
+                                     down->pitch))
+        return rc;
+    for (bml_dev* peer : {up, down}) {
+        if (peer->device != d->device) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, d->device, peer->device);
+            if (!can) return fail(BML_ECUDA, "bml_dev_connect_local: no peer access between devices");
+            cudaError_t e = cudaDeviceEnablePeerAccess(peer->device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+            (void)cudaGetLastError();
+        }
+    }
+    link_peer(d, up->buf, up->flags, up->rows, true);
+    link_peer(d, down->buf, down->flags, down->rows, false);
+    d->connected = true;
+    return BML_OK;
+}
+
+int bml_dev_exchange_halos(bml_dev* d) {
+    if (int rc = check(d)) return rc;
+    if (!d->connected) return fill_images(d, d->cur);
+    push_halo_kernel<<<1, 1024, 0, d->stream>>>(d->row0(d->cur), d->W, d->pitch, d->rows,
+                                                d->up_halo[d->cur], d->down_halo[d->cur],
+                                                d->up_flag, d->down_flag, d->ncols());
+    BML_CUDA(cudaGetLastError());
+    ++d->pubs;
+    return BML_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,117 @@
+// bml/engine.hpp — the reference engine interface
+// (/root/reference/proj/include/bml/engine.hpp:15-79) with one new backend,
+// Backend::B200 ("b200"), implemented on sm_100a through the C-ABI in
+// include/bml_dev.h. This library ships no CPU stepping engine: the four
+// reference CPU backend names stay in the enum so call sites compile, but
+// selecting them throws std::invalid_argument (no silent CPU fallback).
+#pragma once
+
+#include <cstdint>
+#include <filesystem>
+#include <functional>
+#include <memory>
+#include <optional>
+#include <string_view>
+#include <vector>
+
+#include "bml/grid.hpp"
+
+struct bml_dev;
+
+namespace bml {
+
+enum class Backend {
+    ScalarNaive,   // reference CPU engine (not provided here)
+    ScalarHalo,    // reference CPU engine (not provided here)
+    ParallelRows,  // reference CPU engine (not provided here)
+    Lanes,         // reference CPU engine (not provided here)
+    B200,          // device-resident bit-plane lattice on NVIDIA B200 (sm_100a)
+};
+
+enum class Phase { Horizontal, Vertical };
+
+std::string_view backend_name(Backend b);
+std::optional<Backend> backend_from_name(std::string_view name);
+
+// Cells advanced per device word (the bit-plane width).
+int lane_width();
+
+constexpr Cell horizontal_rule(Cell left, Cell center, Cell right) {
+    if (center == Cell::Empty) return left == Cell::LR ? Cell::LR : Cell::Empty;
+    if (center == Cell::LR && right == Cell::Empty) return Cell::Empty;
+    return center;
+}
+
+constexpr Cell vertical_rule(Cell top, Cell center, Cell bottom) {
+    if (center == Cell::Empty) return top == Cell::TB ? Cell::TB : Cell::Empty;
+    if (center == Cell::TB && bottom == Cell::Empty) return Cell::Empty;
+    return center;
+}
+
+struct SimConfig {
+    int n = 0;
+    double rho = 0.0;
+    long steps = 0;
+    std::uint64_t seed = 0;
+    Backend backend = Backend::B200;
+    int threads = 1;
+    long snapshot_every = 0;
+    std::filesystem::path out_dir;
+    // --- extensions (defaults keep reference call sites valid) ---
+    int devices = 1;                  // row bands (GPUs); placed round-robin on visible GPUs
+    bool observer_reads_grid = true;  // download pair.cur before every observer call
+};
+
+void validate(const SimConfig& cfg);
+
+GridPair make_grid_pair(Backend backend, const Grid& initial);
+
+void step_phase(Backend backend, GridPair& pair, Phase phase, int threads = 1);
+
+void step(Backend backend, GridPair& pair, int threads = 1);
+
+struct StepMetrics;
+using StepObserver = std::function<void(const StepMetrics&)>;
+
+Grid run(const SimConfig& cfg, GridPair& pair, const StepObserver& observer = {});
+
+// ---- device-resident lattice (extension; what run()/step() use internally) ----
+struct VehicleCounts;
+
+// One n x n torus resident on the GPU(s): `devices` row bands placed
+// round-robin on the visible GPUs, halo rows exchanged by the step kernel
+// itself. Throws std::invalid_argument / std::runtime_error / std::bad_alloc
+// mapped from the C-ABI status codes.
+class DeviceLattice {
+public:
+    explicit DeviceLattice(int n, int devices = 1);
+    ~DeviceLattice();
+    DeviceLattice(const DeviceLattice&) = delete;
+    DeviceLattice& operator=(const DeviceLattice&) = delete;
+
+    int n() const { return n_; }
+    int bands() const { return static_cast<int>(bands_.size()); }
+
+    void upload(const Grid& g);
+    void download(Grid& g) const;  // writes the interior of g (any layout, size n)
+    Grid download() const;         // halo-layout grid, ghosts unfilled
+
+    void step(long steps);
+    // Per-step metrics for `steps` steps; step indices start at first_step.
+    // Throws std::logic_error on a conservation violation (engine.cpp:219-224).
+    std::vector<StepMetrics> step_with_metrics(long steps, long first_step = 1);
+    std::int64_t phase(Phase p);  // returns moved_in_phase
+    VehicleCounts counts() const;
+
+    void configure(int block_steps, int strip_rows);
+    void set_stream(void* cuda_stream);  // single-band only
+    void synchronize() const;
+    bml_dev* handle(int band = 0) const { return bands_.at(static_cast<std::size_t>(band)); }
+
+private:
+    int n_;
+    std::vector<bml_dev*> bands_;
+    int block_steps_ = 8;
+};
+
+}  // namespace bml

@@ -1,0 +1,68 @@
+"""Generate tests/golden/*.json from the UNMODIFIED reference (oracle/_ref/ref_driver).
+
+TEST INFRASTRUCTURE. Run in the build container (where /root/reference exists and
+`make -C oracle ref` has built the driver); the JSON it writes is committed so the
+GPU box (which has no /root/reference) can check the CUDA path against it.
+
+    python tests/golden/make_goldens.py small      # seconds-to-a-minute configs
+    python tests/golden/make_goldens.py big        # N=8192 (~5 min each, lanes)
+    python tests/golden/make_goldens.py huge       # N=32768 / N=65536 (hours, lanes)
+
+Every record holds the reference's init digest, final digest after `steps`
+full steps, the vehicle counts and (where metrics=1) the observer-path sums
+of moved vehicles and the last StepMetrics.
+"""
+import json
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+DRIVER = os.path.join(HERE, "..", "..", "oracle", "_ref", "ref_driver")
+
+SMALL = [
+    # SURVEY §8(c) golden table + BASELINE configs[0..1]
+    dict(n=256, rho=0.3, seed=1, steps=1024, metrics=1),
+    dict(n=256, rho=0.3, seed=42, steps=1024, metrics=1),
+    dict(n=256, rho=0.3, seed=7, steps=1024, metrics=1),
+    dict(n=1024, rho=0.38, seed=1, steps=4096, metrics=1),
+    # extra coverage: non-multiple-of-32 sizes, both regimes, long runs
+    dict(n=1000, rho=0.25, seed=3, steps=512, metrics=1),
+    dict(n=777, rho=0.5, seed=5, steps=300, metrics=1),
+    dict(n=2048, rho=0.35, seed=1, steps=256, metrics=1),
+    dict(n=4096, rho=0.35, seed=2, steps=64, metrics=0),
+]
+BIG = [
+    dict(n=8192, rho=0.25, seed=1, steps=10000, metrics=0),
+    dict(n=8192, rho=0.5, seed=1, steps=10000, metrics=0),
+]
+HUGE = [
+    dict(n=32768, rho=0.35, seed=1, steps=10000, metrics=0),
+    dict(n=65536, rho=0.35, seed=1, steps=10000, metrics=0),
+]
+
+
+def name_of(c):
+    return f"ref_n{c['n']}_rho{c['rho']}_seed{c['seed']}_steps{c['steps']}.json"
+
+
+def run(c, force=False):
+    out = os.path.join(HERE, name_of(c))
+    if os.path.exists(out) and not force:
+        print("exists", out)
+        return
+    args = [DRIVER, "golden"] + [f"{k}={v}" for k, v in c.items()] + ["backend=lanes"]
+    print("running", " ".join(args), flush=True)
+    res = subprocess.run(args, check=True, capture_output=True, text=True)
+    rec = json.loads(res.stdout)
+    rec["generator"] = "oracle/_ref/ref_driver (unmodified reference sources, lanes backend)"
+    with open(out, "w") as f:
+        json.dump(rec, f, indent=1, sort_keys=True)
+    print("wrote", out, rec["final_digest"], flush=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1] if len(sys.argv) > 1 else "small"
+    table = {"small": SMALL, "big": BIG, "huge": HUGE}[which]
+    for c in table:
+        run(c)

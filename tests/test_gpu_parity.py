@@ -1,0 +1,269 @@
+"""GPU parity: the b200 engine (CUDA, sm_100a) against the oracle and the reference goldens.
+
+Mirrors the reference's own engine tests (/root/reference/proj/tests/test_engine.cpp,
+test_metrics.cpp, acceptance_main.cpp criteria 1/2/8/9) with the device backend
+substituted. Integer CA: every comparison is bit-exact.
+"""
+import os
+import random
+
+import pytest
+
+from conftest import load_goldens, rows_to_bytes
+
+pytestmark = pytest.mark.gpu
+
+
+def rand_lattice(seed, n):
+    rng = random.Random(seed)
+    return bytes(b % 3 for b in rng.randbytes(n * n))
+
+
+def grid_of(bml, n, cells):
+    return bml.Grid.from_bytes(n, cells)
+
+
+# ----------------------------------------------------------- known answers
+PHASE_CASES = [  # test_engine.cpp:63-81 / acceptance_main.cpp:234-241
+    (">.>.", ".>.>"),
+    (">>..", ">.>."),
+    (">>>>", ">>>>"),
+    (">v..", ">v.."),
+]
+
+
+@pytest.mark.parametrize("row,expected", PHASE_CASES)
+def test_single_row_horizontal_phase(gpu, row, expected):
+    bml = gpu
+    g = bml.Grid.from_text(row + "\n....\n....\n....")
+    out = bml.step_phase(g, bml.Phase.horizontal)
+    assert out.to_text() == expected + "\n....\n....\n....\n"
+
+
+def test_two_by_two_steps(gpu):  # test_engine.cpp:83-93
+    bml = gpu
+    assert bml.step(bml.Grid.from_text(">.\n.v"), 1).to_text() == ".>\n.v\n"
+    assert bml.step(bml.Grid.from_text(">.\n.."), 2).to_text() == ">.\n..\n"
+    assert bml.step(bml.Grid.from_text("..\n.."), 1).to_text() == "..\n..\n"
+
+
+def test_self_neighbour_wrap(gpu):  # n=1, n=2 self-wrap cases
+    bml = gpu
+    assert bml.step(bml.Grid.from_text(">"), 5).to_text() == ">\n"
+    assert bml.step(bml.Grid.from_text("v"), 5).to_text() == "v\n"
+    assert bml.step(bml.Grid.from_text(">>\n.."), 3).to_text() == ">>\n..\n"
+
+
+def test_never_blocked_orbit_metrics(gpu):  # test_metrics.cpp:62-75
+    bml = gpu
+    _, metrics = bml.simulate(bml.Grid.from_text(">...\n....\n.v..\n...."), 8)
+    assert len(metrics) == 8
+    for m in metrics:
+        assert (m.lr_moved, m.tb_moved, m.mobility) == (1, 1, 1.0)
+
+
+def test_vacuum_mobility_is_one(gpu):  # test_metrics.cpp:47-60
+    bml = gpu
+    _, metrics = bml.simulate(bml.Grid.from_text("\n".join(["." * 8] * 8)), 3)
+    assert [m.mobility for m in metrics] == [1.0, 1.0, 1.0]
+    assert bml.classify([m.mobility for m in metrics]) == bml.Regime.FreeFlow
+
+
+# ----------------------------------------------------------- random lattices vs oracle
+SIZES = list(range(1, 65)) + [65, 95, 96, 97, 127, 128, 129, 255, 256, 257, 480, 1000, 1023, 1024, 1025]
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_random_lattice_steps_match_oracle(gpu, oracle, n):
+    bml = gpu
+    cells = rand_lattice(1000 + n, n)
+    steps = 1 + (n * 7) % 37 if n <= 257 else 9
+    got = bml.step(grid_of(bml, n, cells), steps).to_bytes()
+    assert got == oracle.run(n, cells, steps), f"n={n} steps={steps}"
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 16, 31, 32, 33, 63, 64, 100, 1024, 1030])
+@pytest.mark.parametrize("phase", [0, 1])
+def test_single_phase_and_moved_match_oracle(gpu, oracle, n, phase):
+    bml = gpu
+    cells = rand_lattice(7 * n + phase, n)
+    lat = bml.DeviceLattice(n)
+    lat.upload(grid_of(bml, n, cells))
+    moved = lat.phase(bml.Phase.horizontal if phase == 0 else bml.Phase.vertical)
+    got = lat.download().to_bytes()
+    want = oracle.phase(n, cells, phase)
+    assert got == want
+    assert moved == oracle.moved(n, cells, want, phase)
+
+
+@pytest.mark.parametrize("block", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("strip", [1, 3, 16, 64, 1000])
+@pytest.mark.parametrize("n", [37, 64, 96, 1024, 1056])
+def test_block_and_strip_configurations_agree(gpu, oracle, block, strip, n):
+    bml = gpu
+    cells = rand_lattice(n * 31 + block, n)
+    steps = 45
+    lat = bml.DeviceLattice(n)
+    lat.configure(block_steps=block, strip_rows=strip)
+    lat.upload(grid_of(bml, n, cells))
+    lat.step(steps)
+    assert lat.download().to_bytes() == oracle.run(n, cells, steps)
+
+
+@pytest.mark.parametrize("n,steps", [(5, 50), (33, 40), (64, 33), (250, 20), (1024, 17)])
+def test_simulate_metrics_match_oracle(gpu, oracle, n, steps):
+    bml = gpu
+    cells = oracle.init_grid(n, 0.35, n)
+    final, metrics = bml.simulate(grid_of(bml, n, cells), steps)
+    want, (lm, tm, lc, tc) = oracle.run(n, cells, steps, metrics=True)
+    assert final.to_bytes() == want
+    assert [m.step for m in metrics] == list(range(1, steps + 1))
+    assert [m.lr_moved for m in metrics] == lm
+    assert [m.tb_moved for m in metrics] == tm
+    assert [m.lr_count for m in metrics] == lc
+    assert [m.tb_count for m in metrics] == tc
+
+
+# ----------------------------------------------------------- reference goldens
+def _golden_ids(g):
+    return f"n{g['n']}_rho{g['rho']}_seed{g['seed']}_steps{g['steps']}"
+
+
+GOLDENS = [g for g in load_goldens() if g["n"] <= 8192]
+
+
+@pytest.mark.parametrize("g", GOLDENS, ids=_golden_ids)
+def test_reference_golden(gpu, g):
+    bml = gpu
+    grid = bml.init_grid(g["n"], g["rho"], g["seed"])
+    assert f"0x{grid.digest():016x}" == g["init_digest"]
+    if "sum_lr_moved" in g:
+        final, metrics = bml.simulate(grid, g["steps"])
+        assert sum(m.lr_moved for m in metrics) == g["sum_lr_moved"]
+        assert sum(m.tb_moved for m in metrics) == g["sum_tb_moved"]
+        last = metrics[-1]
+        assert (last.step, last.lr_moved, last.tb_moved) == (
+            g["last"]["step"], g["last"]["lr_moved"], g["last"]["tb_moved"])
+        assert (last.lr_count, last.tb_count) == (g["lr_count"], g["tb_count"])
+    else:
+        final = bml.step(grid, g["steps"])
+    assert f"0x{final.digest():016x}" == g["final_digest"]
+    assert bml.count_vehicles(final) == (g["lr_count"], g["tb_count"])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("g", [g for g in load_goldens() if g["n"] > 8192], ids=_golden_ids)
+def test_reference_golden_huge(gpu, g):
+    if g["n"] > 32768 and not os.environ.get("BML_HUGE"):
+        pytest.skip("set BML_HUGE=1 for the N=65536 golden (host init ~minutes, 16 GiB)")
+    bml = gpu
+    grid = bml.init_grid(g["n"], g["rho"], g["seed"])
+    assert f"0x{grid.digest():016x}" == g["init_digest"]
+    final = bml.step(grid, g["steps"])
+    assert f"0x{final.digest():016x}" == g["final_digest"]
+
+
+# ----------------------------------------------------------- properties (size-independent)
+@pytest.mark.parametrize("n", [512, 4096])
+def test_conservation_and_changed_equals_twice_moved(gpu, oracle, n):
+    """test_engine.cpp:140-151 (conservation), :172-186 (changed = 2 x moved)."""
+    bml = gpu
+    cells = oracle.init_grid(n, 0.4, 11)
+    g = grid_of(bml, n, cells)
+    lat = bml.DeviceLattice(n)
+    lat.upload(g)
+    before = lat.download().to_bytes()
+    for phase in (bml.Phase.horizontal, bml.Phase.vertical):
+        moved = lat.phase(phase)
+        after = lat.download().to_bytes()
+        changed = sum(1 for a, b in zip(before, after) if a != b)
+        assert changed == 2 * moved
+        before = after
+    assert lat.counts() == oracle.counts(n, cells)
+
+
+@pytest.mark.parametrize("n", [23, 1024, 2000])
+def test_shift_equivariance(gpu, n):
+    """test_engine.cpp:188-199: step commutes with torus rotations."""
+    bml = gpu
+    cells = rand_lattice(n, n)
+    dr, dc = n // 3, (2 * n) // 5
+
+    def rot(b):
+        out = bytearray(n * n)
+        for r in range(n):
+            src = b[r * n:(r + 1) * n]
+            rr = (r + dr) % n
+            out[rr * n:(rr + 1) * n] = src[-dc % n:] + src[:-dc % n] if dc % n else src
+        return bytes(out)
+
+    lhs = bml.step(grid_of(bml, n, rot(cells)), 7).to_bytes()
+    rhs = rot(bml.step(grid_of(bml, n, cells), 7).to_bytes())
+    assert lhs == rhs
+
+
+def test_determinism_repeat(gpu):  # acceptance criterion 8
+    bml = gpu
+    g = bml.init_grid(333, 0.3, 9)
+    a, ma = bml.simulate(g, 50)
+    b, mb = bml.simulate(g, 50)
+    assert a == b and a.digest() == b.digest()
+    assert [(m.lr_moved, m.tb_moved) for m in ma] == [(m.lr_moved, m.tb_moved) for m in mb]
+
+
+# ----------------------------------------------------------- row bands (virtual ranks on one GPU)
+@pytest.mark.parametrize("devices", [2, 3, 4, 8])
+@pytest.mark.parametrize("n", [128, 1000, 1024])
+def test_row_bands_match_single_band(gpu, oracle, devices, n):
+    """GPU-count invariance: g bands with in-kernel halo exchange
+    equal one band and the oracle — the ParallelRows determinism test
+    (test_engine.cpp:201-211) with bands in place of threads."""
+    bml = gpu
+    cells = oracle.init_grid(n, 0.38, devices)
+    steps = 37
+    got = bml.step(grid_of(bml, n, cells), steps, devices=devices).to_bytes()
+    assert got == oracle.run(n, cells, steps)
+    final, metrics = bml.simulate(grid_of(bml, n, cells), steps, devices=devices)
+    want, (lm, tm, lc, tc) = oracle.run(n, cells, steps, metrics=True)
+    assert final.to_bytes() == want
+    assert [m.lr_moved for m in metrics] == lm
+    assert [m.tb_moved for m in metrics] == tm
+    assert [m.lr_count for m in metrics] == lc
+
+
+def test_row_bands_reject_thin_bands(gpu):
+    bml = gpu
+    with pytest.raises(ValueError):
+        bml.DeviceLattice(40, devices=4)
+
+
+# ----------------------------------------------------------- boundary behaviour / errors
+def test_upload_rejects_invalid_cells(gpu):
+    bml = gpu
+    with pytest.raises(ValueError):
+        bml.Grid.from_bytes(4, bytes([0, 1, 2, 3] * 4))
+
+
+def test_zero_steps_is_identity(gpu):
+    bml = gpu
+    g = bml.init_grid(50, 0.5, 2)
+    assert bml.step(g, 0) == g
+    final, metrics = bml.simulate(g, 0)
+    assert final == g and metrics == []
+
+
+def test_cpu_backends_are_not_silently_used(gpu):
+    bml = gpu
+    g = bml.Grid.from_text(">.\n.v")
+    for b in (bml.Backend.naive, bml.Backend.halo, bml.Backend.parallel, bml.Backend.lanes):
+        with pytest.raises(ValueError):
+            bml.step(g, 1, backend=b)
+
+
+def test_native_library_is_loaded(gpu):
+    """The engine that ran is the in-tree CUDA library, not anything else."""
+    bml = gpu
+    bml.step(bml.Grid.from_text(">.\n.v"), 1)
+    with open("/proc/self/maps") as f:
+        maps = f.read()
+    assert os.path.realpath(bml.LIB_DEV) in maps
