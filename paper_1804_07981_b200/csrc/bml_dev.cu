@@ -157,6 +157,17 @@ __device__ __forceinline__ uint2 load_cells(const uint2* row, int word, int c0, 
 
 __device__ __forceinline__ void put(uint2* p, uint32_t l, uint32_t t) { *p = make_uint2(l, t); }
 
+// Asynchronous 8-byte global->shared copies (LDGSTS) feeding a per-warp ring of
+// input rows, so each warp keeps kRing-1 rows of loads in flight.
+constexpr int kRing = 8;
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // ------------------------------------------------------- temporally blocked step
 //
 // Warp w handles (strip, col). Lane l stands for the 32 cells starting at
@@ -167,52 +178,155 @@ __device__ __forceinline__ void put(uint2* p, uint32_t l, uint32_t t) { *p = mak
 // Software pipeline: stage s (step s+1 of the block) at loop index j consumes
 // row j-2s at time s (produced by stage s-1 one iteration earlier, so all K
 // stages of an iteration are independent) and emits row j-2s-1 at time s+1.
-// Stage K-1 therefore emits row j-2K+1 at time K.
+// Stage K-1 therefore emits row j-2K+1 at time K. The loop is unrolled by two
+// and the TB window's two T registers swap roles by iteration parity, so the
+// loop-carried state never moves between registers.
+template <int K>
+struct PipeState {
+    uint32_t pl[K + 1], pt[K + 1];  // stage inputs, one iteration old
+    uint32_t ts[K][2];              // T after LR of the two previous rows (parity slots)
+    uint32_t eB[K], lB[K];          // E and L after LR of the previous row
+    uint32_t cm[K], cc[K];          // packed 16-bit counters (COUNT only)
+};
+
+struct StripCtx {
+    int lane, r_lo, r_hi, out_word;
+    uint32_t valid;
+};
+
+// Final-stage output of row o: the row itself plus its ghost images (the
+// band's own ghost rows for a single band, or the neighbours' ghost rows for
+// connected bands). Aligned modes have n >= 32 > kHalo, so each row has at
+// most one image per side and every store is a predicated STG (no branches
+// around the shuffles of the next stage).
+template <int K, int MODE, bool COUNT>
+__device__ __forceinline__ void store_row(const StepArgs& a, const StripCtx& c, int o, uint32_t l,
+                                          uint32_t t) {
+    const bool row_ok = o >= c.r_lo && o < c.r_hi;
+    const bool st = row_ok && c.valid != 0u;
+    const uint2 v = make_uint2(l & c.valid, t & c.valid);
+    const long long off = static_cast<long long>(o) * a.pitch + c.out_word;
+    if (MODE == kGeneric) {
+        if (st) {
+            a.dst[off] = v;
+            if (a.single_band) {
+                for (int h = o - a.n; h >= -kHalo; h -= a.n)
+                    a.dst[static_cast<long long>(h) * a.pitch + c.out_word] = v;
+                for (int h = o + a.n; h < a.rows + kHalo; h += a.n)
+                    a.dst[static_cast<long long>(h) * a.pitch + c.out_word] = v;
+            } else {
+                if (o < kHalo) a.up_halo[off] = v;
+                if (o >= a.rows - kHalo) a.down_halo[off - static_cast<long long>(a.rows) * a.pitch] = v;
+            }
+        }
+        return;
+    }
+    if (st) a.dst[off] = v;
+    uint2* top_img = a.single_band ? a.dst + static_cast<long long>(a.rows) * a.pitch : a.up_halo;
+    uint2* bot_img = a.single_band ? a.dst - static_cast<long long>(a.rows) * a.pitch
+                                   : a.down_halo - static_cast<long long>(a.rows) * a.pitch;
+    if (st && o < kHalo) top_img[off] = v;              // row o -> ghost row rows+o (or up peer)
+    if (st && o >= a.rows - kHalo) bot_img[off] = v;    // row o -> ghost row o-rows (or down peer)
+}
+
+template <int K, int MODE, bool COUNT, int P>
+__device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const int j,
+                                          const StepArgs& a, const StripCtx& c) {
+#pragma unroll
+    for (int s = K - 1; s >= 0; --s) {
+        const uint32_t L = (s == 0) ? x.x : q.pl[s];
+        const uint32_t T = (s == 0) ? x.y : q.pt[s];
+        // ---- LR phase on row rho = j - 2s
+        const uint32_t E = ~(L | T);
+        uint32_t Ll, Er;
+        if (MODE == kFullRow) {
+            Ll = __shfl_sync(kFull, L, (c.lane + 31) & 31);
+            Er = __shfl_sync(kFull, E, (c.lane + 1) & 31);
+        } else {
+            Ll = __shfl_up_sync(kFull, L, 1);
+            Er = __shfl_down_sync(kFull, E, 1);
+        }
+        const uint32_t prevL = __funnelshift_l(Ll, L, 1);
+        const uint32_t nextE = __funnelshift_r(E, Er, 1);
+        const uint32_t vac = L & nextE;
+        const uint32_t Lp = (prevL & E) | (L ^ vac);
+        const uint32_t Ep = ~(Lp | T);
+        // ---- TB phase emits row rho - 1
+        const uint32_t tA = q.ts[s][P];
+        const uint32_t tB = q.ts[s][P ^ 1];
+        const uint32_t vacT = tB & Ep;
+        const uint32_t newT = (tA & q.eB[s]) | (tB ^ vacT);
+        const uint32_t newL = q.lB[s];
+        if (COUNT) {
+            const int rho = j - 2 * s;
+            const unsigned span = static_cast<unsigned>(c.r_hi - c.r_lo);
+            if (static_cast<unsigned>(rho - c.r_lo) < span) q.cm[s] += __popc(vac & c.valid);
+            if (static_cast<unsigned>(rho - 1 - c.r_lo) < span) {
+                q.cm[s] += static_cast<uint32_t>(__popc(vacT & c.valid)) << 16;
+                q.cc[s] += __popc(newL & c.valid) +
+                           (static_cast<uint32_t>(__popc(newT & c.valid)) << 16);
+            }
+        }
+        q.ts[s][P] = T;  // becomes tB next iteration; old tB becomes tA
+        q.eB[s] = Ep;
+        q.lB[s] = Lp;
+        if (s < K - 1) {
+            q.pl[s + 1] = newL;
+            q.pt[s + 1] = newT;
+        } else {
+            store_row<K, MODE, COUNT>(a, c, j - 2 * K + 1, newL, newT);
+        }
+    }
+}
+
 template <int K, int MODE, bool COUNT>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 step_block_kernel(const StepArgs a) {
     const int lane = threadIdx.x & 31;
     const int warps_total = gridDim.x * kWarpsPerCta;
+    __shared__ uint2 ring[kWarpsPerCta][kRing][32];
+    uint2 (*my_ring)[32] = ring[threadIdx.x >> 5];
+
     for (int item = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5); item < a.items;
          item += warps_total) {
         const int strip = item / a.ncols;
         const int col = item - strip * a.ncols;
-        const int r_lo = strip * a.strip_rows;
-        const int r_hi = (strip == a.nstrips - 1) ? a.rows : r_lo + a.strip_rows;
+        StripCtx c;
+        c.lane = lane;
+        c.r_lo = strip * a.strip_rows;
+        c.r_hi = (strip == a.nstrips - 1) ? a.rows : c.r_lo + a.strip_rows;
 
-        int word = lane, c0 = 0, out_word = lane;
-        uint32_t valid = kFull;
+        int word = lane, c0 = 0;
+        c.out_word = lane;
+        c.valid = kFull;
         if (MODE != kFullRow) {
             const int w = col * kOutWords + lane - 1;
             const bool is_out = lane >= 1 && lane <= kOutWords && w < a.W;
-            out_word = w;
-            valid = is_out ? (w == a.W - 1 ? a.last_mask : kFull) : 0u;
+            c.out_word = w;
+            c.valid = is_out ? (w == a.W - 1 ? a.last_mask : kFull) : 0u;
             word = ((w % a.W) + a.W) % a.W;
             long long cc = (32LL * w) % a.n;
             if (cc < 0) cc += a.n;
             c0 = static_cast<int>(cc);
         }
 
-        const bool top_strip = r_lo == 0;
-        const bool bot_strip = r_hi == a.rows;
         if (!a.single_band) {
-            if (top_strip) wait_flag(a.top_flag, a.expect, a.error_flag);
-            if (bot_strip) wait_flag(a.bot_flag, a.expect, a.error_flag);
+            if (c.r_lo == 0) wait_flag(a.top_flag, a.expect, a.error_flag);
+            if (c.r_hi == a.rows) wait_flag(a.bot_flag, a.expect, a.error_flag);
         }
 
-        uint32_t pl[K + 1], pt[K + 1];           // stage inputs, one iteration old
-        uint32_t tA[K], tB[K], eB[K], lB[K];     // per-stage TB window
-        uint32_t cm[K], cc[K];                   // packed 16-bit counters
+        PipeState<K> q;
 #pragma unroll
         for (int s = 0; s < K; ++s) {
-            pl[s] = pt[s] = tA[s] = tB[s] = eB[s] = lB[s] = 0u;
-            cm[s] = cc[s] = 0u;
+            q.pl[s] = q.pt[s] = q.ts[s][0] = q.ts[s][1] = q.eB[s] = q.lB[s] = 0u;
+            q.cm[s] = q.cc[s] = 0u;
         }
-        pl[K] = pt[K] = 0u;
+        q.pl[K] = q.pt[K] = 0u;
 
-        const int j_begin = r_lo - K;
-        const int j_load_end = r_hi + K;
-        const int j_end = r_hi + 2 * K - 1;
+        const int j_begin = c.r_lo - K;
+        const int j_load_end = c.r_hi + K;
+        // r_hi + 2K - 1 iterations end the pipeline; round up to an even count
+        const int j_end = j_begin + (((c.r_hi + 2 * K - 1 - j_begin) + 1) & ~1);
         const bool coherent = !a.single_band;
 
         auto fetch = [&](int j) -> uint2 {
@@ -220,87 +334,56 @@ step_block_kernel(const StepArgs a) {
             const uint2* row = a.src + static_cast<long long>(j) * a.pitch;
             return load_cells<MODE>(row, word, c0, a.n, coherent && (j < 0 || j >= a.rows));
         };
+        auto issue = [&](int j) {
+            if (j < j_load_end)
+                cp_async8(&my_ring[(j - j_begin) & (kRing - 1)][lane],
+                          a.src + static_cast<long long>(j) * a.pitch + word);
+            cp_async_commit();
+        };
+        auto next_row = [&](int j, uint2& nx0, uint2& nx1) -> uint2 {
+            uint2 x;
+            if (MODE == kGeneric) {
+                x = nx0;
+                nx0 = nx1;
+                nx1 = fetch(j + 2);
+            } else {
+                cp_async_wait<kRing - 2>();
+                x = my_ring[(j - j_begin) & (kRing - 1)][lane];
+                issue(j + kRing - 1);
+            }
+            return x;
+        };
 
-        uint2 nx0 = fetch(j_begin);
-        uint2 nx1 = fetch(j_begin + 1);
-        for (int j = j_begin; j < j_end; ++j) {
-            const uint2 x = nx0;
-            nx0 = nx1;
-            nx1 = fetch(j + 2);
+        uint2 nx0 = make_uint2(0u, 0u), nx1 = make_uint2(0u, 0u);
+        if (MODE == kGeneric) {
+            nx0 = fetch(j_begin);
+            nx1 = fetch(j_begin + 1);
+        } else {
+            __syncwarp();
 #pragma unroll
-            for (int s = K - 1; s >= 0; --s) {
-                const uint32_t L = (s == 0) ? x.x : pl[s];
-                const uint32_t T = (s == 0) ? x.y : pt[s];
-                // ---- LR phase on row rho = j - 2s
-                const uint32_t E = ~(L | T);
-                uint32_t Ll, Er;
-                if (MODE == kFullRow) {
-                    Ll = __shfl_sync(kFull, L, (lane + 31) & 31);
-                    Er = __shfl_sync(kFull, E, (lane + 1) & 31);
-                } else {
-                    Ll = __shfl_up_sync(kFull, L, 1);
-                    Er = __shfl_down_sync(kFull, E, 1);
-                }
-                const uint32_t prevL = __funnelshift_l(Ll, L, 1);
-                const uint32_t nextE = __funnelshift_r(E, Er, 1);
-                const uint32_t vac = L & nextE;
-                const uint32_t Lp = (prevL & E) | (L ^ vac);
-                const uint32_t Ep = ~(Lp | T);
-                // ---- TB phase emits row rho - 1
-                const uint32_t vacT = tB[s] & Ep;
-                const uint32_t newT = (tA[s] & eB[s]) | (tB[s] ^ vacT);
-                const uint32_t newL = lB[s];
-                if (COUNT) {
-                    const int rho = j - 2 * s;
-                    if (static_cast<unsigned>(rho - r_lo) < static_cast<unsigned>(r_hi - r_lo))
-                        cm[s] += __popc(vac & valid);
-                    if (static_cast<unsigned>(rho - 1 - r_lo) < static_cast<unsigned>(r_hi - r_lo)) {
-                        cm[s] += static_cast<uint32_t>(__popc(vacT & valid)) << 16;
-                        cc[s] += __popc(newL & valid) +
-                                 (static_cast<uint32_t>(__popc(newT & valid)) << 16);
-                    }
-                }
-                tA[s] = tB[s];
-                tB[s] = T;
-                eB[s] = Ep;
-                lB[s] = Lp;
-                if (s < K - 1) {
-                    pl[s + 1] = newL;
-                    pt[s + 1] = newT;
-                } else {
-                    const int o = j - 2 * K + 1;
-                    if (o >= r_lo) {
-                        const uint32_t ol = newL & valid, ot = newT & valid;
-                        if (valid) {
-                            put(a.dst + static_cast<long long>(o) * a.pitch + out_word, ol, ot);
-                            if (a.single_band) {
-                                for (int h = o - a.n; h >= -kHalo; h -= a.n)
-                                    put(a.dst + static_cast<long long>(h) * a.pitch + out_word, ol, ot);
-                                for (int h = o + a.n; h < a.rows + kHalo; h += a.n)
-                                    put(a.dst + static_cast<long long>(h) * a.pitch + out_word, ol, ot);
-                            } else {
-                                if (o < kHalo)
-                                    put(a.up_halo + static_cast<long long>(o) * a.pitch + out_word, ol, ot);
-                                if (o >= a.rows - kHalo)
-                                    put(a.down_halo + static_cast<long long>(o - a.rows) * a.pitch + out_word, ol, ot);
-                            }
-                        }
-                        if (!a.single_band) {
-                            if (o == kHalo - 1) publish(a.up_flag);
-                            if (o == a.rows - 1) publish(a.down_flag);
-                        }
-                    }
-                }
+            for (int i = 0; i < kRing - 1; ++i) issue(j_begin + i);
+        }
+        for (int j = j_begin; j < j_end; j += 2) {
+            const uint2 x0 = next_row(j, nx0, nx1);
+            pipe_iter<K, MODE, COUNT, 0>(q, x0, j, a, c);
+            const uint2 x1 = next_row(j + 1, nx0, nx1);
+            pipe_iter<K, MODE, COUNT, 1>(q, x1, j + 1, a, c);
+            if (!a.single_band) {
+                // rows j-2K+1 and j-2K+2 were just stored
+                const int o1 = j - 2 * K + 2;
+                if ((o1 == kHalo - 1 || o1 == kHalo) && c.r_lo == 0) publish(a.up_flag);
+                if ((o1 == a.rows - 1 || o1 == a.rows) && c.r_hi == a.rows) publish(a.down_flag);
             }
         }
 
+        if (MODE != kGeneric) cp_async_wait<0>();
         if (COUNT) {
 #pragma unroll
             for (int s = 0; s < K; ++s) {
-                const unsigned v0 = __reduce_add_sync(kFull, cm[s] & 0xffffu);
-                const unsigned v1 = __reduce_add_sync(kFull, cm[s] >> 16);
-                const unsigned v2 = __reduce_add_sync(kFull, cc[s] & 0xffffu);
-                const unsigned v3 = __reduce_add_sync(kFull, cc[s] >> 16);
+                const unsigned v0 = __reduce_add_sync(kFull, q.cm[s] & 0xffffu);
+                const unsigned v1 = __reduce_add_sync(kFull, q.cm[s] >> 16);
+                const unsigned v2 = __reduce_add_sync(kFull, q.cc[s] & 0xffffu);
+                const unsigned v3 = __reduce_add_sync(kFull, q.cc[s] >> 16);
                 if (lane == 0) {
                     unsigned long long* m = a.metrics + a.step_base + s;
                     if (v0) atomicAdd(m, static_cast<unsigned long long>(v0));
