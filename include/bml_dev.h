@@ -104,8 +104,17 @@ int bml_dev_set_stream(bml_dev *dev, void *stream);
 int bml_dev_sync(bml_dev *dev);
 
 /* Tuning knobs (0 = keep current): temporal block depth (full steps fused per
- * launch, 1..16) and rows per strip. */
+ * launch / ghost depth of the resident kernel, 1..16, default 16) and rows per
+ * warp strip of the streaming kernel (1..1000, -1 = automatic, the default). */
 int bml_dev_configure(bml_dev *dev, int block_steps, int strip_rows);
+
+/* Small lattices (n % 32 == 0, n <= 1024) run the whole step loop in one
+ * cluster-resident kernel (lattice kept in registers of a thread-block cluster,
+ * DSMEM ghost-row exchange) unless disabled: mode 1 = auto (default), 0 = always
+ * use the streaming kernel. bml_dev_path() reports the cluster size used by the
+ * last bml_dev_step (0 = streaming kernel). */
+int bml_dev_set_resident(bml_dev *dev, int mode);
+int bml_dev_path(bml_dev *dev, int *resident_cluster);
 
 /* Kernel statistics since the last reset: launches of the step kernels and
  * their summed device time (CUDA events around each launch; enable first). */

@@ -26,6 +26,7 @@
 // and below the band, which the kernel itself refreshes for the NEXT launch
 // (directly into a neighbour GPU's buffer over NVLink for row bands).
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -396,6 +397,174 @@ step_block_kernel(const StepArgs a) {
     }
 }
 
+// ------------------------------------------------------------ resident cluster kernel
+//
+// Small lattices (n % 32 == 0, W = n/32 <= 32) are latency-bound in the
+// streaming kernel (a few microseconds of work per launch). Here ONE thread-
+// block cluster keeps the whole lattice in registers for the entire run:
+// CTA c of C owns rows [c*B, (c+1)*B), B = n/C, and additionally carries
+// G ghost rows above and below (its "extended window", E = B + 2G rows,
+// RPW rows per warp, lane = word). Each step is computed on the whole
+// window in registers; adjacent warps exchange one boundary row per phase
+// through shared memory (one __syncthreads per step). Every G steps the CTAs
+// refresh their ghost rows from the neighbours' shared memory (DSMEM) behind
+// one cluster barrier, so cross-SM synchronisation happens once per G steps.
+struct ResidentArgs {
+    const uint2* src;
+    uint2* dst;
+    int n, W, pitch;
+    int ghost;   // G
+    long long steps;
+    unsigned long long* metrics;
+    int metrics_stride;
+};
+
+constexpr int kResidentMaxWarps = 32;
+constexpr int kResidentMaxGhost = 16;
+
+template <int RPW, bool COUNT>
+__global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int C = static_cast<int>(cluster.num_blocks());
+    const int c = static_cast<int>(cluster.block_rank());
+    const int G = a.ghost;
+    const int B = a.n / C;
+    const int r0 = c * B;
+    const int NW = blockDim.x >> 5;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int W = a.W;
+    const bool lane_ok = lane < W;
+    const int left = lane == 0 ? W - 1 : lane - 1;
+    const int right = lane + 1 >= W ? 0 : lane + 1;
+
+    __shared__ uint32_t xT[2][kResidentMaxWarps][32];  // last row's T of each warp
+    __shared__ uint32_t xO[2][kResidentMaxWarps][32];  // first row's occupancy after LR
+    __shared__ uint2 exportb[2][2 * kResidentMaxGhost][32];
+    __shared__ unsigned long long cnt[4][kResidentMaxGhost];
+
+    uint32_t L[RPW], T[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int e = w * RPW + i;
+        int row = (r0 - G + e) % a.n;
+        if (row < 0) row += a.n;
+        const uint2 x = lane_ok ? a.src[static_cast<long long>(row) * a.pitch + lane] : make_uint2(0u, 0u);
+        L[i] = x.x;
+        T[i] = x.y;
+    }
+    if (COUNT && threadIdx.x < 4 * kResidentMaxGhost) (&cnt[0][0])[threadIdx.x] = 0ull;
+
+    const uint32_t valid = lane_ok ? kFull : 0u;
+    int par = 0, bp = 0;
+    for (long long done = 0; done < a.steps;) {
+        const int kb = static_cast<int>(min(static_cast<long long>(G), a.steps - done));
+        if (done > 0) {
+            // ghost rows from the neighbours' exports of the previous block
+            const uint2* up = cluster.map_shared_rank(&exportb[bp ^ 1][0][0], (c + C - 1) % C);
+            const uint2* dn = cluster.map_shared_rank(&exportb[bp ^ 1][0][0], (c + 1) % C);
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int e = w * RPW + i;
+                if (e < G) {  // neighbour above: its last G owned rows live at export rows [G, 2G)
+                    const uint2 x = up[(G + e) * 32 + lane];
+                    L[i] = x.x;
+                    T[i] = x.y;
+                } else if (e >= G + B) {  // neighbour below: its first G owned rows
+                    const uint2 x = dn[(e - G - B) * 32 + lane];
+                    L[i] = x.x;
+                    T[i] = x.y;
+                }
+            }
+        }
+        for (int s = 0; s < kb; ++s) {
+            uint32_t Op[RPW];
+            uint32_t lr_moved = 0;
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {  // LR phase, row-local
+                const uint32_t O = L[i] | T[i];
+                const uint32_t Ll = __shfl_sync(kFull, L[i], left);
+                const uint32_t Or = __shfl_sync(kFull, O, right);
+                const uint32_t prevL = __funnelshift_l(Ll, L[i], 1);
+                const uint32_t nextO = __funnelshift_r(O, Or, 1);
+                const uint32_t inc = prevL & ~O;
+                const uint32_t vac = L[i] & ~nextO;
+                if (COUNT) {
+                    const int e = w * RPW + i;
+                    if (e >= G && e < G + B) lr_moved += __popc(vac & valid);
+                }
+                L[i] = inc | (L[i] & nextO);
+                Op[i] = L[i] | T[i];
+            }
+            xT[par][w][lane] = T[RPW - 1];
+            xO[par][w][lane] = Op[0];
+            __syncthreads();
+            const uint32_t t_up = w > 0 ? xT[par][w - 1][lane] : 0u;
+            const uint32_t o_dn = w < NW - 1 ? xO[par][w + 1][lane] : kFull;
+            uint32_t tb_moved = 0, lr_cnt = 0, tb_cnt = 0;
+#pragma unroll
+            for (int i = RPW - 1; i >= 0; --i) {  // TB phase, top-down neighbours
+                const uint32_t above = i > 0 ? T[i - 1] : t_up;
+                const uint32_t below = i < RPW - 1 ? Op[i + 1] : o_dn;
+                const uint32_t nt = (above & ~Op[i]) | (T[i] & below);
+                if (COUNT) {
+                    const int e = w * RPW + i;
+                    if (e >= G && e < G + B) {
+                        tb_moved += __popc(T[i] & ~below & valid);
+                        lr_cnt += __popc(L[i] & valid);
+                        tb_cnt += __popc(nt & valid);
+                    }
+                }
+                T[i] = nt;
+            }
+            if (COUNT) {
+                const unsigned v0 = __reduce_add_sync(kFull, lr_moved);
+                const unsigned v1 = __reduce_add_sync(kFull, tb_moved);
+                const unsigned v2 = __reduce_add_sync(kFull, lr_cnt);
+                const unsigned v3 = __reduce_add_sync(kFull, tb_cnt);
+                if (lane == 0) {
+                    if (v0) atomicAdd(&cnt[0][s], static_cast<unsigned long long>(v0));
+                    if (v1) atomicAdd(&cnt[1][s], static_cast<unsigned long long>(v1));
+                    if (v2) atomicAdd(&cnt[2][s], static_cast<unsigned long long>(v2));
+                    if (v3) atomicAdd(&cnt[3][s], static_cast<unsigned long long>(v3));
+                }
+            }
+            par ^= 1;
+        }
+        // publish owned boundary rows: export rows [0,G) = first G owned, [G,2G) = last G owned
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int e = w * RPW + i;
+            if (e >= G && e < 2 * G) exportb[bp][e - G][lane] = make_uint2(L[i], T[i]);
+            if (e >= B && e < B + G) exportb[bp][G + (e - B)][lane] = make_uint2(L[i], T[i]);
+        }
+        if (COUNT) {
+            __syncthreads();
+            if (threadIdx.x < 4 * kb) {
+                const int q = threadIdx.x / kb, s = threadIdx.x % kb;
+                const unsigned long long v = cnt[q][s];
+                if (v) atomicAdd(a.metrics + static_cast<long long>(q) * a.metrics_stride + done + s, v);
+                cnt[q][s] = 0ull;
+            }
+        }
+        cluster.sync();
+        bp ^= 1;
+        done += kb;
+    }
+    // owned rows back to global, plus the single-band ghost images
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int e = w * RPW + i;
+        if (e >= G && e < G + B && lane_ok) {
+            const int row = r0 + e - G;
+            const uint2 v = make_uint2(L[i], T[i]);
+            a.dst[static_cast<long long>(row) * a.pitch + lane] = v;
+            for (int h = row - a.n; h >= -kHalo; h -= a.n) a.dst[static_cast<long long>(h) * a.pitch + lane] = v;
+            for (int h = row + a.n; h < a.n + kHalo; h += a.n) a.dst[static_cast<long long>(h) * a.pitch + lane] = v;
+        }
+    }
+}
+
 // ------------------------------------------------------------ single phases
 // One thread per (row, word) of the band; used by step_phase (bml_dev_phase).
 struct PhaseArgs {
@@ -619,8 +788,10 @@ struct bml_dev {
     int device = 0;
     uint32_t last_mask = kFull;
     int mode = kGeneric;
-    int block_steps = 8;
-    int strip_rows = 256;
+    int block_steps = 16;
+    int strip_rows = 0;      // 0 = auto (auto_strip_rows)
+    int resident = 1;        // 1: use the cluster-resident kernel when the lattice qualifies
+    int resident_cluster = 0;  // cluster size actually used by the last resident launch
     int sms = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
@@ -732,7 +903,6 @@ int create_common(int n, int row_begin, int row_end, int device, bml_dev** out) 
     d->last_mask = nb == 32 ? kFull : ((1u << nb) - 1u);
     d->mode = (n % 32 != 0) ? kGeneric : (d->W == 32 ? kFullRow : kAligned);
     cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, device);
-    if (d->single_band() && n <= 2048) d->strip_rows = std::max(16, n / 64);
 
     auto bail = [&](cudaError_t err, const char* what) {
         bml_dev_destroy(d);
@@ -774,10 +944,25 @@ int check_errors(bml_dev* d) {
     return BML_OK;
 }
 
+// Rows per warp strip. Each strip re-reads 2K ghost rows and runs K-1 drain
+// iterations, so longer strips waste less, but the grid needs enough warps
+// (~12 per SM resident) to keep the ALU pipes busy. Measured on B200
+// (profiles/r1_sweep_streaming.jsonl): n=8192 -> 64..128, n=32768 -> 256.
+int auto_strip_rows(const bml_dev* d, int k) {
+    if (d->strip_rows > 0) return d->strip_rows;
+    const long long cols = d->ncols();
+    const long long target_warps = 30LL * d->sms;  // ~2.5 waves of 12 resident warps/SM
+    int r = 1000;
+    while (r > 2 * k + 16 && cols * (d->rows / r) < target_warps) r /= 2;
+    r = std::max(r, std::min(d->rows, std::max(16, 4 * k)));
+    if (d->connected) r = std::max(r, kHalo);
+    return std::min(r, 1000);
+}
+
 int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_stride) {
     StepKernel kern = pick(k, d->mode, count);
     if (!kern) return fail(BML_EINVAL, "unsupported block depth " + std::to_string(k));
-    const int strip = d->strip_rows;
+    const int strip = auto_strip_rows(d, k);
     // floor: every strip has >= strip_rows rows (the last absorbs the
     // remainder), so the ghost-row sources of a band never straddle strips
     const int nstrips = std::max(1, d->rows / strip);
@@ -829,6 +1014,110 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
     ++d->launches;
     d->cur ^= 1;
     if (d->connected) ++d->pubs;
+    return BML_OK;
+}
+
+using ResidentKernel = void (*)(const ResidentArgs);
+
+template <bool COUNT>
+ResidentKernel pick_resident(int rpw) {
+    switch (rpw) {
+        case 1: return resident_kernel<1, COUNT>;
+        case 2: return resident_kernel<2, COUNT>;
+        case 3: return resident_kernel<3, COUNT>;
+        case 4: return resident_kernel<4, COUNT>;
+        case 5: return resident_kernel<5, COUNT>;
+        case 6: return resident_kernel<6, COUNT>;
+        case 8: return resident_kernel<8, COUNT>;
+        default: return nullptr;
+    }
+}
+
+// Geometry of the resident launch, or false if the lattice does not qualify.
+bool resident_plan(const bml_dev* d, int cluster, int* ghost, int* rpw, int* warps) {
+    if (!d->resident || !d->single_band() || d->connected) return false;
+    if (d->n % 32 != 0 || d->W > 32 || d->n % cluster != 0) return false;
+    const int B = d->n / cluster;
+    const int G = std::min(kResidentMaxGhost, std::max(1, d->block_steps));
+    if (B < G) return false;
+    const int E = B + 2 * G;
+    for (int r : {5, 4, 6, 3, 8, 2, 1}) {
+        if (E % r == 0 && E / r <= kResidentMaxWarps && E / r >= 1) {
+            *ghost = G;
+            *rpw = r;
+            *warps = E / r;
+            return true;
+        }
+    }
+    return false;
+}
+
+int launch_resident(bml_dev* d, long long steps, bool count, bool* used) {
+    *used = false;
+    for (int cluster : {16, 8, 4, 2, 1}) {
+        int G = 0, rpw = 0, nw = 0;
+        if (!resident_plan(d, cluster, &G, &rpw, &nw)) continue;
+        ResidentKernel kern = count ? pick_resident<true>(rpw) : pick_resident<false>(rpw);
+        if (!kern) continue;
+        if (cluster > 8) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                cudaSuccess) {
+                (void)cudaGetLastError();
+                continue;
+            }
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(cluster));
+        cfg.blockDim = dim3(static_cast<unsigned>(32 * nw));
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = d->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int max_clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
+            (void)cudaGetLastError();
+            continue;
+        }
+        ResidentArgs ra{};
+        ra.src = d->row0(d->cur);
+        ra.dst = d->row0(d->cur ^ 1);
+        ra.n = d->n;
+        ra.W = d->W;
+        ra.pitch = d->pitch;
+        ra.ghost = G;
+        ra.steps = steps;
+        ra.metrics = d->metrics;
+        ra.metrics_stride = static_cast<int>(steps);
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (d->timing) {
+            e0 = take_event(d);
+            e1 = take_event(d);
+            cudaEventRecord(e0, d->stream);
+        }
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ra);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            if (d->timing) {
+                d->ev_pool.push_back(e0);
+                d->ev_pool.push_back(e1);
+            }
+            continue;
+        }
+        if (d->timing) {
+            cudaEventRecord(e1, d->stream);
+            d->pending.emplace_back(e0, e1);
+        }
+        ++d->launches;
+        d->cur ^= 1;
+        d->resident_cluster = cluster;
+        *used = true;
+        return BML_OK;
+    }
     return BML_OK;
 }
 
@@ -906,12 +1195,26 @@ int bml_dev_configure(bml_dev* d, int block_steps, int strip_rows) {
         d->block_steps = block_steps;
     }
     if (strip_rows) {
-        if (strip_rows < 1 || strip_rows > 1000)
-            return fail(BML_EINVAL, "strip_rows must be in [1, 1000]");
-        if (d->connected && strip_rows < kHalo)
+        if (strip_rows < -1 || strip_rows > 1000)
+            return fail(BML_EINVAL, "strip_rows must be in [1, 1000] (or -1 for auto)");
+        if (strip_rows == -1) strip_rows = 0;
+        if (d->connected && strip_rows > 0 && strip_rows < kHalo)
             return fail(BML_EINVAL, "connected bands need strip_rows >= 16");
         d->strip_rows = strip_rows;
     }
+    return BML_OK;
+}
+
+int bml_dev_set_resident(bml_dev* d, int mode) {
+    if (int rc = check(d)) return rc;
+    if (mode != 0 && mode != 1) return fail(BML_EINVAL, "bml_dev_set_resident: mode must be 0 or 1");
+    d->resident = mode;
+    return BML_OK;
+}
+
+int bml_dev_path(bml_dev* d, int* resident_cluster) {
+    if (!d) return fail(BML_EINVAL, "null bml_dev handle");
+    if (resident_cluster) *resident_cluster = d->resident_cluster;
     return BML_OK;
 }
 
@@ -1056,7 +1359,10 @@ int bml_dev_step(bml_dev* d, int64_t steps, int64_t* lr_moved, int64_t* tb_moved
         if (int rc = ensure_metrics(d, steps)) return rc;
         BML_CUDA(cudaMemsetAsync(d->metrics, 0, 4 * steps * sizeof(unsigned long long), d->stream));
     }
-    long long done = 0;
+    d->resident_cluster = 0;
+    bool resident_used = false;
+    if (int rc = launch_resident(d, steps, count, &resident_used)) return rc;
+    long long done = resident_used ? steps : 0;
     while (done < steps) {
         const int k = largest_block_at_most(steps - done, d->block_steps);
         if (int rc = launch_block(d, k, count, static_cast<int>(done), static_cast<int>(steps)))
@@ -1137,7 +1443,7 @@ int validate_neighbours(bml_dev* d, int up_end, int up_n, int up_pitch, int dn_b
         return fail(BML_EINVAL, "bml_dev_connect: up neighbour does not end where this band begins");
     if (dn_begin != d->row_end % d->n)
         return fail(BML_EINVAL, "bml_dev_connect: down neighbour does not begin where this band ends");
-    if (d->strip_rows < kHalo) d->strip_rows = kHalo;
+    if (d->strip_rows > 0 && d->strip_rows < kHalo) d->strip_rows = kHalo;
     return BML_OK;
 }
 

@@ -234,6 +234,16 @@ void DeviceLattice::configure(int block_steps, int strip_rows) {
     if (block_steps) block_steps_ = block_steps;
 }
 
+void DeviceLattice::set_resident(bool enabled) {
+    for (bml_dev* h : bands_) ok(bml_dev_set_resident(h, enabled ? 1 : 0), "bml_dev_set_resident");
+}
+
+int DeviceLattice::resident_cluster() const {
+    int c = 0;
+    ok(bml_dev_path(bands_[0], &c), "bml_dev_path");
+    return c;
+}
+
 void DeviceLattice::set_stream(void* cuda_stream) {
     if (bands_.size() != 1) throw std::invalid_argument("set_stream: single-band lattices only");
     ok(bml_dev_set_stream(bands_[0], cuda_stream), "bml_dev_set_stream");

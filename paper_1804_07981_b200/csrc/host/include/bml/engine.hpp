@@ -104,6 +104,10 @@ public:
     VehicleCounts counts() const;
 
     void configure(int block_steps, int strip_rows);
+    // Small-lattice cluster-resident kernel: enabled by default; resident_cluster()
+    // reports the cluster size the last step() used (0 = streaming kernel).
+    void set_resident(bool enabled);
+    int resident_cluster() const;
     void set_stream(void* cuda_stream);  // single-band only
     void synchronize() const;
     bml_dev* handle(int band = 0) const { return bands_.at(static_cast<std::size_t>(band)); }

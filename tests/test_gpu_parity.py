@@ -267,3 +267,45 @@ def test_native_library_is_loaded(gpu):
     with open("/proc/self/maps") as f:
         maps = f.read()
     assert os.path.realpath(bml.LIB_DEV) in maps
+
+
+# ----------------------------------------------------------- cluster-resident small-lattice kernel
+@pytest.mark.parametrize("n", [32, 64, 96, 128, 160, 256, 512, 640, 992, 1024])
+@pytest.mark.parametrize("ghost", [1, 2, 4, 8, 16])
+def test_resident_kernel_matches_oracle(gpu, oracle, n, ghost):
+    bml = gpu
+    cells = oracle.init_grid(n, 0.38, n + ghost)
+    steps = 53
+    lat = bml.DeviceLattice(n)
+    lat.configure(block_steps=ghost)
+    lat.upload(bml.Grid.from_bytes(n, cells))
+    metrics = lat.step_with_metrics(steps)
+    assert lat.resident_cluster > 0, "resident kernel did not run"
+    want, (lm, tm, lc, tc) = oracle.run(n, cells, steps, metrics=True)
+    assert lat.download().to_bytes() == want
+    assert [m.lr_moved for m in metrics] == lm
+    assert [m.tb_moved for m in metrics] == tm
+    assert [m.lr_count for m in metrics] == lc
+    assert [m.tb_count for m in metrics] == tc
+    # bare loop (no counters) and the streaming kernel agree
+    lat.upload(bml.Grid.from_bytes(n, cells))
+    lat.step(steps)
+    assert lat.download().to_bytes() == want
+    lat.set_resident(False)
+    lat.upload(bml.Grid.from_bytes(n, cells))
+    lat.step(steps)
+    assert lat.resident_cluster == 0
+    assert lat.download().to_bytes() == want
+
+
+def test_resident_kernel_long_run_golden(gpu):
+    """configs[1] (N=1024, rho=.38, 4096 steps) through the resident kernel."""
+    bml = gpu
+    g = [x for x in load_goldens() if x["n"] == 1024][0]
+    lat = bml.DeviceLattice(1024)
+    lat.upload(bml.init_grid(1024, g["rho"], g["seed"]))
+    metrics = lat.step_with_metrics(g["steps"])
+    assert lat.resident_cluster > 0
+    assert f"0x{lat.download().digest():016x}" == g["final_digest"]
+    assert sum(m.lr_moved for m in metrics) == g["sum_lr_moved"]
+    assert sum(m.tb_moved for m in metrics) == g["sum_tb_moved"]
