@@ -58,61 +58,59 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    NVML (nvidia_ml_py) is polled every ~2 ms from a thread, so even a
+    millisecond-scale timed region gets samples; falls back to nvidia-smi -lms.
+    """
+
+    REASONS = {  # nvmlClocksEventReason bits
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.thread = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((sm, rs))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
             self.thread.start()
-        except OSError:
-            self.proc = None
+        except Exception:
+            self.thread = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self.thread:
             self.thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[3:7]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        reasons = sorted({k for _, r in self.samples for k, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm for sm, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
 
 
 # ---------------------------------------------------------------- C-ABI (ctypes)
@@ -378,7 +376,97 @@ def run_e2e(abi, torch, bml, grid, n, steps, args):
 
 
 def run_b200_multi(args, wl):
-    raise SystemExit("multi-GPU bench: see bench_multi in a later revision")
+    """One process per GPU (torchrun): each rank owns a row band of a weak-scaled
+    square lattice (~world x the cells of the N=1 workload, side a multiple of 32);
+    neighbours exchange ghost rows inside the step kernel over NVLink (CUDA IPC
+    peer stores + flags). torch.distributed only bootstraps and reduces timings."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1804_07981_b200 as bml
+    from paper_1804_07981_b200.dist import BandLattice, weak_scaled_n
+
+    n1, rho, seed, steps, desc = wl
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    n = weak_scaled_n(n1, world)
+    cells = bml.init_grid(n, rho, seed).to_bytes()  # same reference-RNG lattice on every rank
+    band = BandLattice(n, rank, world, local, block_steps=args.block, strip_rows=args.strip)
+    stream = torch.cuda.Stream(device=dev)
+    band.set_stream(stream.cuda_stream)
+    band.upload_rows(cells[band.begin * n: band.end * n])
+    band.exchange_halos()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            band.step(steps)
+    stream.synchronize()
+    band.enable_timing(True)
+    band.kernel_stats(reset=True)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.fill_(i & 0xFF)
+                starts[i].record(stream)
+                band.step(steps)
+                ends[i].record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        wall = time.perf_counter() - t0
+    launches, kms = band.kernel_stats(reset=True)
+    my_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t = torch.tensor([my_ms, kms / max(1, launches)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, avg_launch_ms = float(t[0]), float(t[1])
+    value = n * n * steps * args.steps / (total_ms / 1e3) / 1e9
+    peak, peak_src = measured_peaks()
+    cells_per_launch = band.rows * n * steps * args.steps / max(1, launches)
+    achieved = BYTES_PER_CELL_UPDATE * cells_per_launch / (avg_launch_ms / 1e3) / 1e9
+    # e2e: each rank uploads its band from pinned host memory, steps, downloads
+    host_in = torch.frombuffer(bytearray(cells[band.begin * n: band.end * n]), dtype=torch.uint8).pin_memory()
+    e2e_times = []
+    for i in range(args.steps):
+        dist.barrier()
+        t1 = time.perf_counter()
+        band.upload_rows(host_in.data_ptr())
+        band.exchange_halos()
+        band.step(steps)
+        band.download_rows()
+        e2e_times.append(time.perf_counter() - t1)
+    et = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        line = {
+            "metric": "Gcell-updates/sec", "value": value, "unit": "Gcell-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic: reference init_grid(n, rho, seed) lattice",
+            "config": {"workload": desc + f" weak-scaled to n={n}", "n": n, "rho": rho, "seed": seed,
+                       "steps_per_run": steps, "parallelism": f"row bands x{world}, NVLink peer ghost rows",
+                       "l2": "flushed (256 MiB write) between bench steps",
+                       "block_steps": args.block, "layout": "bit-planes, 2 bits/cell"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "step_block_kernel",
+                         "peak_source": peak_src, "launches_per_rank": launches,
+                         "avg_launch_us": avg_launch_ms * 1e3},
+            "cpu_baseline": None,
+            "e2e": {"value": n * n * steps * args.steps / float(et[0]) / 1e9, "unit": "Gcell-updates/s",
+                    "h2d_bytes_per_step": n * n, "d2h_bytes_per_step": n * n},
+            "gpu_launches": launches * world, "wall_s": wall, "clocks": clocks.summary(),
+        }
+        print(json.dumps(line))
+    band.close()
+    dist.destroy_process_group()
 
 
 def main():
@@ -388,8 +476,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c1")
-    ap.add_argument("--block", type=int, default=16)
-    ap.add_argument("--strip", type=int, default=0)
+    ap.add_argument("--block", type=int, default=16, help="steps fused per launch / resident ghost depth")
+    ap.add_argument("--strip", type=int, default=0, help="streaming-kernel rows per strip (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

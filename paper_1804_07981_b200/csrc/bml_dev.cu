@@ -453,7 +453,10 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
         L[i] = x.x;
         T[i] = x.y;
     }
-    if (COUNT && threadIdx.x < 4 * kResidentMaxGhost) (&cnt[0][0])[threadIdx.x] = 0ull;
+    if (COUNT) {
+        for (int i = threadIdx.x; i < 4 * kResidentMaxGhost; i += blockDim.x) (&cnt[0][0])[i] = 0ull;
+        __syncthreads();
+    }
 
     const uint32_t valid = lane_ok ? kFull : 0u;
     int par = 0, bp = 0;
@@ -540,8 +543,8 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
         }
         if (COUNT) {
             __syncthreads();
-            if (threadIdx.x < 4 * kb) {
-                const int q = threadIdx.x / kb, s = threadIdx.x % kb;
+            for (int t = threadIdx.x; t < 4 * kb; t += blockDim.x) {
+                const int q = t / kb, s = t % kb;
                 const unsigned long long v = cnt[q][s];
                 if (v) atomicAdd(a.metrics + static_cast<long long>(q) * a.metrics_stride + done + s, v);
                 cnt[q][s] = 0ull;
