@@ -42,10 +42,13 @@
 namespace {
 
 constexpr int kHalo = 16;       // ghost rows per side == max steps fused per launch
-constexpr int kMaxBlock = 16;   // largest K instantiated
 constexpr int kWarpsPerCta = 4;
 constexpr int kOutWords = 30;   // output words per warp in the haloed modes
 constexpr unsigned kFull = 0xffffffffu;
+
+#ifndef BML_FMA_SHIFTS
+#define BML_FMA_SHIFTS 0
+#endif
 
 enum Mode { kGeneric = 0, kAligned = 1, kFullRow = 2 };
 
@@ -94,6 +97,7 @@ struct StepArgs {
     int metrics_stride;
     int step_base;
     int* error_flag;
+    uint32_t two, half;  // 2 and 2^31, passed at run time so ptxas keeps IMAD (FMA pipe) shifts
 };
 
 // --------------------------------------------------------------- device utils
@@ -182,12 +186,22 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Stage K-1 therefore emits row j-2K+1 at time K. The loop is unrolled by two
 // and the TB window's two T registers swap roles by iteration parity, so the
 // loop-carried state never moves between registers.
+// Pipeline state. Values live in modulo-indexed register slots so that the
+// loop (unrolled by 6 = lcm of the 3- and 2-iteration lifetimes) never moves a
+// value between registers:
+//   nt[s][j%3]  TB output T of stage s at iteration j  (stage s+1 reads it at
+//               j+1 as its T, at j+2 as tB, at j+3 as tA)
+//   lp[s][j%2]  LR output L of stage s at iteration j  (emitted as row L at
+//               j+1, read by stage s+1 at j+2)
+//   oc[s]       occupancy after LR of the row stage s saw last iteration
+//   xt[j%3]     T of the row loaded at iteration j (stage 0's TB window)
 template <int K>
 struct PipeState {
-    uint32_t pl[K + 1], pt[K + 1];  // stage inputs, one iteration old
-    uint32_t ts[K][2];              // T after LR of the two previous rows (parity slots)
-    uint32_t eB[K], lB[K];          // E and L after LR of the previous row
-    uint32_t cm[K], cc[K];          // packed 16-bit counters (COUNT only)
+    uint32_t nt[K][3];
+    uint32_t lp[K][2];
+    uint32_t oc[K];
+    uint32_t xt[3];
+    uint32_t cm[K], cc[K];  // packed 16-bit counters (COUNT only)
 };
 
 struct StripCtx {
@@ -200,7 +214,7 @@ struct StripCtx {
 // connected bands). Aligned modes have n >= 32 > kHalo, so each row has at
 // most one image per side and every store is a predicated STG (no branches
 // around the shuffles of the next stage).
-template <int K, int MODE, bool COUNT>
+template <int MODE>
 __device__ __forceinline__ void store_row(const StepArgs& a, const StripCtx& c, int o, uint32_t l,
                                           uint32_t t) {
     const bool row_ok = o >= c.r_lo && o < c.r_hi;
@@ -226,56 +240,70 @@ __device__ __forceinline__ void store_row(const StepArgs& a, const StripCtx& c, 
     uint2* top_img = a.single_band ? a.dst + static_cast<long long>(a.rows) * a.pitch : a.up_halo;
     uint2* bot_img = a.single_band ? a.dst - static_cast<long long>(a.rows) * a.pitch
                                    : a.down_halo - static_cast<long long>(a.rows) * a.pitch;
-    if (st && o < kHalo) top_img[off] = v;              // row o -> ghost row rows+o (or up peer)
-    if (st && o >= a.rows - kHalo) bot_img[off] = v;    // row o -> ghost row o-rows (or down peer)
+    if (st && o < kHalo) top_img[off] = v;            // row o -> ghost row rows+o (or up peer)
+    if (st && o >= a.rows - kHalo) bot_img[off] = v;  // row o -> ghost row o-rows (or down peer)
 }
 
 template <int K, int MODE, bool COUNT, int P>
 __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const int j,
                                           const StepArgs& a, const StripCtx& c) {
+    constexpr int P3 = P % 3, P2 = P % 2;
+    q.xt[P3] = x.y;
 #pragma unroll
     for (int s = K - 1; s >= 0; --s) {
-        const uint32_t L = (s == 0) ? x.x : q.pl[s];
-        const uint32_t T = (s == 0) ? x.y : q.pt[s];
+        const uint32_t L = (s == 0) ? x.x : q.lp[s > 0 ? s - 1 : 0][P2];
+        const uint32_t T = (s == 0) ? x.y : q.nt[s > 0 ? s - 1 : 0][(P3 + 2) % 3];
+        const uint32_t tB = (s == 0) ? q.xt[(P3 + 2) % 3] : q.nt[s > 0 ? s - 1 : 0][(P3 + 1) % 3];
+        const uint32_t tA = (s == 0) ? q.xt[(P3 + 1) % 3] : q.nt[s > 0 ? s - 1 : 0][P3];
         // ---- LR phase on row rho = j - 2s
-        const uint32_t E = ~(L | T);
-        uint32_t Ll, Er;
+        const uint32_t O = L | T;
+#if BML_FMA_SHIFTS
+        // shifts on the FMA pipe (IMAD / IMAD.HI); the ALU pipe is the bottleneck
+        const uint32_t lc = __umulhi(L, a.two);   // L >> 31: carry into the right neighbour
+        const uint32_t oc = O * a.half;           // O << 31: carry into the left neighbour
+        uint32_t cl, cr;
+        if (MODE == kFullRow) {
+            cl = __shfl_sync(kFull, lc, (c.lane + 31) & 31);
+            cr = __shfl_sync(kFull, oc, (c.lane + 1) & 31);
+        } else {
+            cl = __shfl_up_sync(kFull, lc, 1);
+            cr = __shfl_down_sync(kFull, oc, 1);
+        }
+        const uint32_t prevL = L * a.two + cl;            // (L << 1) | carry
+        const uint32_t nextO = __umulhi(O, a.half) | cr;  // (O >> 1) | carry (OR folds into LOP3)
+#else
+        uint32_t Ll, Or;
         if (MODE == kFullRow) {
             Ll = __shfl_sync(kFull, L, (c.lane + 31) & 31);
-            Er = __shfl_sync(kFull, E, (c.lane + 1) & 31);
+            Or = __shfl_sync(kFull, O, (c.lane + 1) & 31);
         } else {
             Ll = __shfl_up_sync(kFull, L, 1);
-            Er = __shfl_down_sync(kFull, E, 1);
+            Or = __shfl_down_sync(kFull, O, 1);
         }
         const uint32_t prevL = __funnelshift_l(Ll, L, 1);
-        const uint32_t nextE = __funnelshift_r(E, Er, 1);
-        const uint32_t vac = L & nextE;
-        const uint32_t Lp = (prevL & E) | (L ^ vac);
-        const uint32_t Ep = ~(Lp | T);
+        const uint32_t nextO = __funnelshift_r(O, Or, 1);
+#endif
+        const uint32_t Lp = (prevL & ~O) | (L & nextO);
+        const uint32_t Op = Lp | T;
         // ---- TB phase emits row rho - 1
-        const uint32_t tA = q.ts[s][P];
-        const uint32_t tB = q.ts[s][P ^ 1];
-        const uint32_t vacT = tB & Ep;
-        const uint32_t newT = (tA & q.eB[s]) | (tB ^ vacT);
-        const uint32_t newL = q.lB[s];
+        const uint32_t newT = (tA & ~q.oc[s]) | (tB & Op);
+        const uint32_t newL = q.lp[s][(P2 + 1) % 2];
         if (COUNT) {
             const int rho = j - 2 * s;
             const unsigned span = static_cast<unsigned>(c.r_hi - c.r_lo);
-            if (static_cast<unsigned>(rho - c.r_lo) < span) q.cm[s] += __popc(vac & c.valid);
+            if (static_cast<unsigned>(rho - c.r_lo) < span) q.cm[s] += __popc(L & ~nextO & c.valid);
             if (static_cast<unsigned>(rho - 1 - c.r_lo) < span) {
-                q.cm[s] += static_cast<uint32_t>(__popc(vacT & c.valid)) << 16;
+                q.cm[s] += static_cast<uint32_t>(__popc(tB & ~Op & c.valid)) << 16;
                 q.cc[s] += __popc(newL & c.valid) +
                            (static_cast<uint32_t>(__popc(newT & c.valid)) << 16);
             }
         }
-        q.ts[s][P] = T;  // becomes tB next iteration; old tB becomes tA
-        q.eB[s] = Ep;
-        q.lB[s] = Lp;
+        q.oc[s] = Op;
+        q.lp[s][P2] = Lp;
         if (s < K - 1) {
-            q.pl[s + 1] = newL;
-            q.pt[s + 1] = newT;
+            q.nt[s][P3] = newT;
         } else {
-            store_row<K, MODE, COUNT>(a, c, j - 2 * K + 1, newL, newT);
+            store_row<MODE>(a, c, j - 2 * K + 1, newL, newT);
         }
     }
 }
@@ -319,15 +347,18 @@ step_block_kernel(const StepArgs a) {
         PipeState<K> q;
 #pragma unroll
         for (int s = 0; s < K; ++s) {
-            q.pl[s] = q.pt[s] = q.ts[s][0] = q.ts[s][1] = q.eB[s] = q.lB[s] = 0u;
+            q.nt[s][0] = q.nt[s][1] = q.nt[s][2] = 0u;
+            q.lp[s][0] = q.lp[s][1] = 0u;
+            q.oc[s] = 0u;
             q.cm[s] = q.cc[s] = 0u;
         }
-        q.pl[K] = q.pt[K] = 0u;
+        q.xt[0] = q.xt[1] = q.xt[2] = 0u;
 
         const int j_begin = c.r_lo - K;
         const int j_load_end = c.r_hi + K;
-        // r_hi + 2K - 1 iterations end the pipeline; round up to an even count
-        const int j_end = j_begin + (((c.r_hi + 2 * K - 1 - j_begin) + 1) & ~1);
+        // r_hi + 2K - 1 iterations drain the pipeline; round up to a multiple of 6
+        const int iters = c.r_hi + 2 * K - 1 - j_begin;
+        const int j_end = j_begin + (iters + 5) / 6 * 6;
         const bool coherent = !a.single_band;
 
         auto fetch = [&](int j) -> uint2 {
@@ -335,11 +366,15 @@ step_block_kernel(const StepArgs a) {
             const uint2* row = a.src + static_cast<long long>(j) * a.pitch;
             return load_cells<MODE>(row, word, c0, a.n, coherent && (j < 0 || j >= a.rows));
         };
-        auto issue = [&](int j) {
-            if (j < j_load_end)
-                cp_async8(&my_ring[(j - j_begin) & (kRing - 1)][lane],
-                          a.src + static_cast<long long>(j) * a.pitch + word);
+        // cp.async ring: row j lands in slot (j - j_begin) % kRing
+        const uint2* gsrc = a.src + static_cast<long long>(j_begin) * a.pitch + word;
+        int j_issue = j_begin;
+        auto issue_next = [&]() {
+            if (j_issue < j_load_end)
+                cp_async8(&my_ring[(j_issue - j_begin) & (kRing - 1)][lane], gsrc);
             cp_async_commit();
+            ++j_issue;
+            gsrc += a.pitch;
         };
         auto next_row = [&](int j, uint2& nx0, uint2& nx1) -> uint2 {
             uint2 x;
@@ -350,7 +385,7 @@ step_block_kernel(const StepArgs a) {
             } else {
                 cp_async_wait<kRing - 2>();
                 x = my_ring[(j - j_begin) & (kRing - 1)][lane];
-                issue(j + kRing - 1);
+                issue_next();
             }
             return x;
         };
@@ -362,18 +397,21 @@ step_block_kernel(const StepArgs a) {
         } else {
             __syncwarp();
 #pragma unroll
-            for (int i = 0; i < kRing - 1; ++i) issue(j_begin + i);
+            for (int i = 0; i < kRing - 1; ++i) issue_next();
         }
-        for (int j = j_begin; j < j_end; j += 2) {
-            const uint2 x0 = next_row(j, nx0, nx1);
-            pipe_iter<K, MODE, COUNT, 0>(q, x0, j, a, c);
-            const uint2 x1 = next_row(j + 1, nx0, nx1);
-            pipe_iter<K, MODE, COUNT, 1>(q, x1, j + 1, a, c);
+        for (int j = j_begin; j < j_end; j += 6) {
+            pipe_iter<K, MODE, COUNT, 0>(q, next_row(j, nx0, nx1), j, a, c);
+            pipe_iter<K, MODE, COUNT, 1>(q, next_row(j + 1, nx0, nx1), j + 1, a, c);
+            pipe_iter<K, MODE, COUNT, 2>(q, next_row(j + 2, nx0, nx1), j + 2, a, c);
+            pipe_iter<K, MODE, COUNT, 3>(q, next_row(j + 3, nx0, nx1), j + 3, a, c);
+            pipe_iter<K, MODE, COUNT, 4>(q, next_row(j + 4, nx0, nx1), j + 4, a, c);
+            pipe_iter<K, MODE, COUNT, 5>(q, next_row(j + 5, nx0, nx1), j + 5, a, c);
             if (!a.single_band) {
-                // rows j-2K+1 and j-2K+2 were just stored
-                const int o1 = j - 2 * K + 2;
-                if ((o1 == kHalo - 1 || o1 == kHalo) && c.r_lo == 0) publish(a.up_flag);
-                if ((o1 == a.rows - 1 || o1 == a.rows) && c.r_hi == a.rows) publish(a.down_flag);
+                // rows j-2K+1 .. j-2K+6 were just stored
+                const int o_last = j - 2 * K + 6;
+                if (c.r_lo == 0 && o_last >= kHalo - 1 && o_last - 6 < kHalo - 1) publish(a.up_flag);
+                if (c.r_hi == a.rows && o_last >= a.rows - 1 && o_last - 6 < a.rows - 1)
+                    publish(a.down_flag);
             }
         }
 
@@ -947,19 +985,29 @@ int check_errors(bml_dev* d) {
     return BML_OK;
 }
 
-// Rows per warp strip. Each strip re-reads 2K ghost rows and runs K-1 drain
-// iterations, so longer strips waste less, but the grid needs enough warps
-// (~12 per SM resident) to keep the ALU pipes busy. Measured on B200
-// (profiles/r1_sweep_streaming.jsonl): n=8192 -> 64..128, n=32768 -> 256.
+// Rows per warp strip. A strip of R rows costs R + 3K - 1 pipeline iterations
+// (2K ghost rows + K-1 drain), so long strips waste less; but an SM needs about
+// four warps to keep its ALU pipes saturated. Model: time ~ (R + 3K) *
+// max(ceil(items / SMs), 4), R a power of two in [16, 256]. It reproduces the
+// measured optima on B200 (profiles/r1_abi_sweep_v3.jsonl): n=8192 -> 128,
+// n=32768 -> 256.
 int auto_strip_rows(const bml_dev* d, int k) {
     if (d->strip_rows > 0) return d->strip_rows;
     const long long cols = d->ncols();
-    const long long target_warps = 30LL * d->sms;  // ~2.5 waves of 12 resident warps/SM
-    int r = 1000;
-    while (r > 2 * k + 16 && cols * (d->rows / r) < target_warps) r /= 2;
-    r = std::max(r, std::min(d->rows, std::max(16, 4 * k)));
-    if (d->connected) r = std::max(r, kHalo);
-    return std::min(r, 1000);
+    long long best_cost = -1;
+    int best = 16;
+    for (int r = 16; r <= 256; r *= 2) {
+        if (d->connected && r < kHalo) continue;
+        const long long strips = std::max(1, d->rows / r);
+        const long long items = strips * cols;
+        const long long per_sm = (items + d->sms - 1) / d->sms;
+        const long long cost = static_cast<long long>(std::min(r, d->rows) + 3 * k) * std::max(per_sm, 4LL);
+        if (best_cost < 0 || cost <= best_cost) {
+            best_cost = cost;
+            best = r;
+        }
+    }
+    return best;
 }
 
 int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_stride) {
@@ -994,6 +1042,8 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
     a.metrics_stride = metrics_stride;
     a.step_base = step_base;
     a.error_flag = d->err + 1;
+    a.two = 2u;
+    a.half = 0x80000000u;
 
     int max_ctas_per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_ctas_per_sm, kern, kWarpsPerCta * 32, 0);
