@@ -49,6 +49,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef BML_FMA_SHIFTS
 #define BML_FMA_SHIFTS 0
 #endif
+#ifndef BML_RES_SKIP
+#define BML_RES_SKIP 0
+#endif
 
 enum Mode { kGeneric = 0, kAligned = 1, kFullRow = 2 };
 
@@ -455,6 +458,7 @@ struct ResidentArgs {
     long long steps;
     unsigned long long* metrics;
     int metrics_stride;
+    int* error_flag;
 };
 
 constexpr int kResidentMaxWarps = 32;
@@ -470,6 +474,7 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
     const int B = a.n / C;
     const int r0 = c * B;
     const int NW = blockDim.x >> 5;
+    const int E = NW * RPW;  // extended window rows = B + 2G
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int W = a.W;
     const bool lane_ok = lane < W;
@@ -478,7 +483,7 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
 
     __shared__ uint32_t xT[2][kResidentMaxWarps][32];  // last row's T of each warp
     __shared__ uint32_t xO[2][kResidentMaxWarps][32];  // first row's occupancy after LR
-    __shared__ uint2 exportb[2][2 * kResidentMaxGhost][32];
+    __shared__ uint2 ghostb[2][2 * kResidentMaxGhost][32];  // [0,G): rows above, [G,2G): rows below
     __shared__ unsigned long long cnt[4][kResidentMaxGhost];
 
     uint32_t L[RPW], T[RPW];
@@ -501,28 +506,39 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
     for (long long done = 0; done < a.steps;) {
         const int kb = static_cast<int>(min(static_cast<long long>(G), a.steps - done));
         if (done > 0) {
-            // ghost rows from the neighbours' exports of the previous block
-            const uint2* up = cluster.map_shared_rank(&exportb[bp ^ 1][0][0], (c + C - 1) % C);
-            const uint2* dn = cluster.map_shared_rank(&exportb[bp ^ 1][0][0], (c + 1) % C);
+            // ghost rows pushed into this CTA's shared memory by the neighbours
+            // before the last cluster barrier (local loads only)
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
                 const int e = w * RPW + i;
-                if (e < G) {  // neighbour above: its last G owned rows live at export rows [G, 2G)
-                    const uint2 x = up[(G + e) * 32 + lane];
+                if (e < G) {
+                    const uint2 x = ghostb[bp ^ 1][e][lane];
                     L[i] = x.x;
                     T[i] = x.y;
-                } else if (e >= G + B) {  // neighbour below: its first G owned rows
-                    const uint2 x = dn[(e - G - B) * 32 + lane];
+                } else if (e >= G + B) {
+                    const uint2 x = ghostb[bp ^ 1][G + (e - G - B)][lane];
                     L[i] = x.x;
                     T[i] = x.y;
                 }
             }
         }
         for (int s = 0; s < kb; ++s) {
+            // ghost rows go stale one row per step from each window edge: a warp
+            // whose rows are all stale skips the arithmetic (warp-uniform)
+#if BML_RES_SKIP
+            const bool live = (w + 1) * RPW > s && w * RPW < E - s;
+#else
+            const bool live = true;
+            (void)E;
+#endif
             uint32_t Op[RPW];
             uint32_t lr_moved = 0;
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {  // LR phase, row-local
+                if (!live) {
+                    Op[i] = 0u;
+                    continue;
+                }
                 const uint32_t O = L[i] | T[i];
                 const uint32_t Ll = __shfl_sync(kFull, L[i], left);
                 const uint32_t Or = __shfl_sync(kFull, O, right);
@@ -545,6 +561,7 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
             uint32_t tb_moved = 0, lr_cnt = 0, tb_cnt = 0;
 #pragma unroll
             for (int i = RPW - 1; i >= 0; --i) {  // TB phase, top-down neighbours
+                if (!live) continue;
                 const uint32_t above = i > 0 ? T[i - 1] : t_up;
                 const uint32_t below = i < RPW - 1 ? Op[i + 1] : o_dn;
                 const uint32_t nt = (above & ~Op[i]) | (T[i] & below);
@@ -572,12 +589,20 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
             }
             par ^= 1;
         }
-        // publish owned boundary rows: export rows [0,G) = first G owned, [G,2G) = last G owned
+        // push owned boundary rows into the neighbours' ghost buffers (DSMEM
+        // stores, made visible by the release/acquire cluster barrier below):
+        // first G owned rows -> the CTA above's rows-below slots, last G owned
+        // rows -> the CTA below's rows-above slots
+        {
+            uint2* up = cluster.map_shared_rank(&ghostb[bp][0][0], (c + C - 1) % C);
+            uint2* dn = cluster.map_shared_rank(&ghostb[bp][0][0], (c + 1) % C);
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-            const int e = w * RPW + i;
-            if (e >= G && e < 2 * G) exportb[bp][e - G][lane] = make_uint2(L[i], T[i]);
-            if (e >= B && e < B + G) exportb[bp][G + (e - B)][lane] = make_uint2(L[i], T[i]);
+            for (int i = 0; i < RPW; ++i) {
+                const int e = w * RPW + i;
+                const uint2 v = make_uint2(L[i], T[i]);
+                if (e >= G && e < 2 * G) up[e * 32 + lane] = v;
+                if (e >= B && e < B + G) dn[(e - B) * 32 + lane] = v;
+            }
         }
         if (COUNT) {
             __syncthreads();
@@ -603,6 +628,189 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
             for (int h = row - a.n; h >= -kHalo; h -= a.n) a.dst[static_cast<long long>(h) * a.pitch + lane] = v;
             for (int h = row + a.n; h < a.n + kHalo; h += a.n) a.dst[static_cast<long long>(h) * a.pitch + lane] = v;
         }
+    }
+}
+
+// ------------------------------------------------------------ resident kernel, p2p variant
+//
+// Same residency as resident_kernel, but no ghost rows: every step the CTA
+// hands its first row's post-LR occupancy to the CTA above and its last row's
+// T plane to the CTA below with st.async remote stores that complete_tx on the
+// receiver's mbarrier (256 B per step per CTA). Only the two boundary warps
+// ever wait, and only for their two neighbours: no cluster-wide barrier, no
+// redundant ghost-row arithmetic.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint32_t bar, uint32_t tx_bytes) {
+    asm volatile(
+        "{ .reg .b64 st; mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1; }" ::"r"(bar),
+        "r"(tx_bytes)
+        : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Bounded wait: a lost handoff raises the error flag after ~2 s instead of
+// hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int* err) {
+    if (mbar_try(bar, parity)) return;
+    if (*reinterpret_cast<volatile int*>(err)) return;  // already failed: do not wait again
+    const long long t0 = clock64();
+    while (!mbar_try(bar, parity)) {
+        if (clock64() - t0 > 4000000000LL) {
+            atomicExch(err, 3);
+            return;
+        }
+    }
+}
+__device__ __forceinline__ void st_async_u32(uint32_t remote_addr, uint32_t v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(remote_addr),
+                 "r"(v), "r"(remote_bar)
+                 : "memory");
+}
+
+template <int RPW, bool COUNT>
+__global__ void __launch_bounds__(1024, 1) resident_p2p_kernel(const ResidentArgs a) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int C = static_cast<int>(cluster.num_blocks());
+    const int c = static_cast<int>(cluster.block_rank());
+    const int B = a.n / C;
+    const int r0 = c * B;
+    const int NW = blockDim.x >> 5;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int W = a.W;
+    const bool lane_ok = lane < W;
+    const int left = lane == 0 ? W - 1 : lane - 1;
+    const int right = lane + 1 >= W ? 0 : lane + 1;
+    const int up_rank = (c + C - 1) % C, dn_rank = (c + 1) % C;
+
+    __shared__ uint32_t xT[2][kResidentMaxWarps][32];
+    __shared__ uint32_t xO[2][kResidentMaxWarps][32];
+    __shared__ uint32_t mT[2][32];  // T of the row above this CTA's first row (from the CTA above)
+    __shared__ uint32_t mO[2][32];  // occupancy after LR of the row below the last row (from below)
+    __shared__ __align__(8) unsigned long long mbar[2];
+    __shared__ unsigned long long cnt[2][4][16];
+
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&mbar[0]), 1);
+        mbar_init(smem_u32(&mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (COUNT)
+        for (int i = threadIdx.x; i < 2 * 4 * 16; i += blockDim.x) (&cnt[0][0][0])[i] = 0ull;
+
+    uint32_t L[RPW], T[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int row = r0 + w * RPW + i;
+        const uint2 x = lane_ok ? a.src[static_cast<long long>(row) * a.pitch + lane] : make_uint2(0u, 0u);
+        L[i] = x.x;
+        T[i] = x.y;
+    }
+    cluster.sync();  // every CTA's mbarriers are initialised before the first remote store
+
+    // remote destinations (constant for the run)
+    const uint32_t up_mO0 = mapa_u32(smem_u32(&mO[0][lane]), up_rank);
+    const uint32_t up_mO1 = mapa_u32(smem_u32(&mO[1][lane]), up_rank);
+    const uint32_t dn_mT0 = mapa_u32(smem_u32(&mT[0][lane]), dn_rank);
+    const uint32_t dn_mT1 = mapa_u32(smem_u32(&mT[1][lane]), dn_rank);
+    const uint32_t up_bar0 = mapa_u32(smem_u32(&mbar[0]), up_rank);
+    const uint32_t up_bar1 = mapa_u32(smem_u32(&mbar[1]), up_rank);
+    const uint32_t dn_bar0 = mapa_u32(smem_u32(&mbar[0]), dn_rank);
+    const uint32_t dn_bar1 = mapa_u32(smem_u32(&mbar[1]), dn_rank);
+    const uint32_t my_bar0 = smem_u32(&mbar[0]), my_bar1 = smem_u32(&mbar[1]);
+
+    const uint32_t valid = lane_ok ? kFull : 0u;
+    for (long long s = 0; s < a.steps; ++s) {
+        const int p = static_cast<int>(s & 1);
+        const uint32_t ph = static_cast<uint32_t>((s >> 1) & 1);
+        const uint32_t my_bar = p ? my_bar1 : my_bar0;
+        if (threadIdx.x == 0) mbar_arm(my_bar, 2 * 32 * 4);
+        uint32_t Op[RPW];
+        uint32_t lr_moved = 0;
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {  // LR phase
+            const uint32_t O = L[i] | T[i];
+            const uint32_t Ll = __shfl_sync(kFull, L[i], left);
+            const uint32_t Or = __shfl_sync(kFull, O, right);
+            const uint32_t prevL = __funnelshift_l(Ll, L[i], 1);
+            const uint32_t nextO = __funnelshift_r(O, Or, 1);
+            if (COUNT) lr_moved += __popc(L[i] & ~nextO & valid);
+            L[i] = (prevL & ~O) | (L[i] & nextO);
+            Op[i] = L[i] | T[i];
+        }
+        if (w == 0) st_async_u32(p ? up_mO1 : up_mO0, Op[0], p ? up_bar1 : up_bar0);
+        if (w == NW - 1) st_async_u32(p ? dn_mT1 : dn_mT0, T[RPW - 1], p ? dn_bar1 : dn_bar0);
+        xT[p][w][lane] = T[RPW - 1];
+        xO[p][w][lane] = Op[0];
+        __syncthreads();
+        if (w == 0 || w == NW - 1) mbar_wait(my_bar, ph, a.error_flag);
+        const uint32_t t_up = w > 0 ? xT[p][w - 1][lane] : mT[p][lane];
+        const uint32_t o_dn = w < NW - 1 ? xO[p][w + 1][lane] : mO[p][lane];
+        uint32_t tb_moved = 0, lr_cnt = 0, tb_cnt = 0;
+#pragma unroll
+        for (int i = RPW - 1; i >= 0; --i) {  // TB phase
+            const uint32_t above = i > 0 ? T[i - 1] : t_up;
+            const uint32_t below = i < RPW - 1 ? Op[i + 1] : o_dn;
+            const uint32_t nt = (above & ~Op[i]) | (T[i] & below);
+            if (COUNT) {
+                tb_moved += __popc(T[i] & ~below & valid);
+                lr_cnt += __popc(L[i] & valid);
+                tb_cnt += __popc(nt & valid);
+            }
+            T[i] = nt;
+        }
+        if (COUNT) {
+            const int chunk = static_cast<int>((s >> 4) & 1), slot = static_cast<int>(s & 15);
+            const unsigned v0 = __reduce_add_sync(kFull, lr_moved);
+            const unsigned v1 = __reduce_add_sync(kFull, tb_moved);
+            const unsigned v2 = __reduce_add_sync(kFull, lr_cnt);
+            const unsigned v3 = __reduce_add_sync(kFull, tb_cnt);
+            if (lane == 0) {
+                if (v0) atomicAdd(&cnt[chunk][0][slot], static_cast<unsigned long long>(v0));
+                if (v1) atomicAdd(&cnt[chunk][1][slot], static_cast<unsigned long long>(v1));
+                if (v2) atomicAdd(&cnt[chunk][2][slot], static_cast<unsigned long long>(v2));
+                if (v3) atomicAdd(&cnt[chunk][3][slot], static_cast<unsigned long long>(v3));
+            }
+            if (slot == 15 || s == a.steps - 1) {
+                __syncthreads();
+                const long long base = s - slot;
+                for (int t = threadIdx.x; t < 4 * (slot + 1); t += blockDim.x) {
+                    const int q = t / (slot + 1), k = t % (slot + 1);
+                    const unsigned long long v = cnt[chunk][q][k];
+                    if (v) atomicAdd(a.metrics + static_cast<long long>(q) * a.metrics_stride + base + k, v);
+                    cnt[chunk][q][k] = 0ull;
+                }
+            }
+        }
+    }
+    cluster.sync();  // no CTA leaves while a neighbour may still address its shared memory
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        if (!lane_ok) continue;
+        const int row = r0 + w * RPW + i;
+        const uint2 v = make_uint2(L[i], T[i]);
+        a.dst[static_cast<long long>(row) * a.pitch + lane] = v;
+        for (int h = row - a.n; h >= -kHalo; h -= a.n) a.dst[static_cast<long long>(h) * a.pitch + lane] = v;
+        for (int h = row + a.n; h < a.n + kHalo; h += a.n) a.dst[static_cast<long long>(h) * a.pitch + lane] = v;
     }
 }
 
@@ -980,7 +1188,8 @@ int check_errors(bml_dev* d) {
     if (e != cudaSuccess) return cuda_fail(e, "error-flag readback");
     if (h[1]) {
         cudaMemsetAsync(d->err, 0, 4 * sizeof(int), d->stream);
-        return fail(BML_ECUDA, "halo flag wait timed out (neighbour band stalled)");
+        return fail(BML_ECUDA, h[1] == 3 ? "resident kernel: DSMEM handoff timed out"
+                                         : "halo flag wait timed out (neighbour band stalled)");
     }
     return BML_OK;
 }
@@ -1073,6 +1282,17 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
 using ResidentKernel = void (*)(const ResidentArgs);
 
 template <bool COUNT>
+ResidentKernel pick_p2p(int rpw) {
+    switch (rpw) {
+        case 1: return resident_p2p_kernel<1, COUNT>;
+        case 2: return resident_p2p_kernel<2, COUNT>;
+        case 4: return resident_p2p_kernel<4, COUNT>;
+        case 8: return resident_p2p_kernel<8, COUNT>;
+        default: return nullptr;
+    }
+}
+
+template <bool COUNT>
 ResidentKernel pick_resident(int rpw) {
     switch (rpw) {
         case 1: return resident_kernel<1, COUNT>;
@@ -1091,6 +1311,17 @@ bool resident_plan(const bml_dev* d, int cluster, int* ghost, int* rpw, int* war
     if (!d->resident || !d->single_band() || d->connected) return false;
     if (d->n % 32 != 0 || d->W > 32 || d->n % cluster != 0) return false;
     const int B = d->n / cluster;
+    if (d->resident == 2) {  // p2p variant: no ghost rows, B = warps * rpw
+        for (int r : {4, 2, 8, 1}) {
+            if (B % r == 0 && B / r <= kResidentMaxWarps) {
+                *ghost = 0;
+                *rpw = r;
+                *warps = B / r;
+                return true;
+            }
+        }
+        return false;
+    }
     const int G = std::min(kResidentMaxGhost, std::max(1, d->block_steps));
     if (B < G) return false;
     const int E = B + 2 * G;
@@ -1110,7 +1341,9 @@ int launch_resident(bml_dev* d, long long steps, bool count, bool* used) {
     for (int cluster : {16, 8, 4, 2, 1}) {
         int G = 0, rpw = 0, nw = 0;
         if (!resident_plan(d, cluster, &G, &rpw, &nw)) continue;
-        ResidentKernel kern = count ? pick_resident<true>(rpw) : pick_resident<false>(rpw);
+        ResidentKernel kern = d->resident == 2
+                                  ? (count ? pick_p2p<true>(rpw) : pick_p2p<false>(rpw))
+                                  : (count ? pick_resident<true>(rpw) : pick_resident<false>(rpw));
         if (!kern) continue;
         if (cluster > 8) {
             if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
@@ -1146,6 +1379,7 @@ int launch_resident(bml_dev* d, long long steps, bool count, bool* used) {
         ra.steps = steps;
         ra.metrics = d->metrics;
         ra.metrics_stride = static_cast<int>(steps);
+        ra.error_flag = d->err + 1;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (d->timing) {
             e0 = take_event(d);
@@ -1260,7 +1494,7 @@ int bml_dev_configure(bml_dev* d, int block_steps, int strip_rows) {
 
 int bml_dev_set_resident(bml_dev* d, int mode) {
     if (int rc = check(d)) return rc;
-    if (mode != 0 && mode != 1) return fail(BML_EINVAL, "bml_dev_set_resident: mode must be 0 or 1");
+    if (mode < 0 || mode > 2) return fail(BML_EINVAL, "bml_dev_set_resident: mode must be 0, 1 or 2");
     d->resident = mode;
     return BML_OK;
 }
@@ -1445,7 +1679,7 @@ int bml_dev_step(bml_dev* d, int64_t steps, int64_t* lr_moved, int64_t* tb_moved
                 }
             }
         }
-        if (d->connected) return check_errors(d);
+        return check_errors(d);
     }
     return BML_OK;
 }

@@ -234,8 +234,8 @@ void DeviceLattice::configure(int block_steps, int strip_rows) {
     if (block_steps) block_steps_ = block_steps;
 }
 
-void DeviceLattice::set_resident(bool enabled) {
-    for (bml_dev* h : bands_) ok(bml_dev_set_resident(h, enabled ? 1 : 0), "bml_dev_set_resident");
+void DeviceLattice::set_resident(int mode) {
+    for (bml_dev* h : bands_) ok(bml_dev_set_resident(h, mode), "bml_dev_set_resident");
 }
 
 int DeviceLattice::resident_cluster() const {

@@ -106,7 +106,7 @@ public:
     void configure(int block_steps, int strip_rows);
     // Small-lattice cluster-resident kernel: enabled by default; resident_cluster()
     // reports the cluster size the last step() used (0 = streaming kernel).
-    void set_resident(bool enabled);
+    void set_resident(int mode);  // 0 = off, 1 = ghost-zone kernel (default), 2 = p2p kernel
     int resident_cluster() const;
     void set_stream(void* cuda_stream);  // single-band only
     void synchronize() const;

@@ -215,7 +215,7 @@ PYBIND11_MODULE(_bml, m) {
              })
         .def("configure", &bml::DeviceLattice::configure, py::arg("block_steps") = 0,
              py::arg("strip_rows") = 0)
-        .def("set_resident", &bml::DeviceLattice::set_resident, py::arg("enabled"))
+        .def("set_resident", &bml::DeviceLattice::set_resident, py::arg("mode"))
         .def_property_readonly("resident_cluster", &bml::DeviceLattice::resident_cluster)
         .def("set_stream",
              [](bml::DeviceLattice& d, std::uintptr_t s) { d.set_stream(reinterpret_cast<void*>(s)); },

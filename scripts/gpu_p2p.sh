@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "resident" -p no:cacheprovider > gpurun_out/pytest_resident.txt 2>&1
+echo "rc=$?" >> gpurun_out/pytest_resident.txt
+timeout 300 python scripts/sweep_resident.py > gpurun_out/sweep_resident3.jsonl 2> gpurun_out/sweep_resident3.err

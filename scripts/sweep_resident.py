@@ -15,7 +15,7 @@ for n, steps in ((1024, 4096), (512, 4096), (256, 4096)):
     stream = torch.cuda.Stream()
     lat.set_stream(stream.cuda_stream)
     for ghost in (1, 2, 4, 8, 16):
-        for resident in (True, False):
+        for resident in (1, 2, 0):
             lat.set_resident(resident)
             lat.configure(block_steps=ghost, strip_rows=16)
             lat.upload(g)

@@ -271,12 +271,13 @@ def test_native_library_is_loaded(gpu):
 
 # ----------------------------------------------------------- cluster-resident small-lattice kernel
 @pytest.mark.parametrize("n", [32, 64, 96, 128, 160, 256, 512, 640, 992, 1024])
-@pytest.mark.parametrize("ghost", [1, 2, 4, 8, 16])
-def test_resident_kernel_matches_oracle(gpu, oracle, n, ghost):
+@pytest.mark.parametrize("ghost,mode", [(1, 1), (2, 1), (4, 1), (8, 1), (16, 1), (16, 2)])
+def test_resident_kernel_matches_oracle(gpu, oracle, n, ghost, mode):
     bml = gpu
     cells = oracle.init_grid(n, 0.38, n + ghost)
     steps = 53
     lat = bml.DeviceLattice(n)
+    lat.set_resident(mode)
     lat.configure(block_steps=ghost)
     lat.upload(bml.Grid.from_bytes(n, cells))
     metrics = lat.step_with_metrics(steps)
@@ -291,7 +292,7 @@ def test_resident_kernel_matches_oracle(gpu, oracle, n, ghost):
     lat.upload(bml.Grid.from_bytes(n, cells))
     lat.step(steps)
     assert lat.download().to_bytes() == want
-    lat.set_resident(False)
+    lat.set_resident(0)
     lat.upload(bml.Grid.from_bytes(n, cells))
     lat.step(steps)
     assert lat.resident_cluster == 0
