@@ -45,6 +45,7 @@ WORKLOADS = {
     "c3": (32768, 0.35, 1, 10000, "configs[3]: N=32768 rho=0.35 10000 steps"),
     "c4": (65536, 0.35, 1, 10000, "configs[4]: N=65536 rho=0.35 10000 steps"),
 }
+DEVICE_INIT_N = 4096  # init_grid on the device from this side up (minutes on the host at 65536)
 BYTES_PER_CELL_UPDATE = 4  # 1 B read + 1 B write per cell per phase
 
 
@@ -237,7 +238,11 @@ def run_b200(args, wl):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    grid = bml.init_grid(n, rho, seed)  # reference RNG path (untimed input generation)
+    # reference RNG path (untimed input generation); large lattices draw it on the
+    # device (bml_dev_init_random, bit-identical to the host shuffle)
+    t_init = time.perf_counter()
+    grid = bml.init_grid(n, rho, seed, on_device=n >= DEVICE_INIT_N)
+    t_init = time.perf_counter() - t_init
     lat = bml.DeviceLattice(n)
     lat.configure(block_steps=args.block, strip_rows=args.strip)
     stream = torch.cuda.Stream(device=dev)
@@ -353,6 +358,8 @@ def run_b200(args, wl):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": timed_launches,
+        "init": {"s": t_init, "where": "device" if n >= DEVICE_INIT_N else "host",
+                 "note": "init_grid incl. readback into a host Grid; untimed input generation"},
         "wall_s": wall,
         "clocks": clocks.summary(),
         "gpu": torch.cuda.get_device_name(dev),
@@ -410,12 +417,13 @@ def run_b200_multi(args, wl):
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     n = weak_scaled_n(n1, world)
-    cells = bml.init_grid(n, rho, seed).to_bytes()  # same reference-RNG lattice on every rank
     band = BandLattice(n, rank, world, local, block_steps=args.block, strip_rows=args.strip)
+    # each rank draws its rows of the same reference-RNG lattice on its own GPU
+    band.init_random(rho, seed)
+    band.exchange_halos()
+    band_cells = band.download_rows()  # host copy of the input, for the e2e leg
     stream = torch.cuda.Stream(device=dev)
     band.set_stream(stream.cuda_stream)
-    band.upload_rows(cells[band.begin * n: band.end * n])
-    band.exchange_halos()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -448,7 +456,7 @@ def run_b200_multi(args, wl):
     cells_per_launch = band.rows * n * steps * args.steps / max(1, launches)
     achieved = BYTES_PER_CELL_UPDATE * cells_per_launch / (avg_launch_ms / 1e3) / 1e9
     # e2e: each rank uploads its band from pinned host memory, steps, downloads
-    host_in = torch.frombuffer(bytearray(cells[band.begin * n: band.end * n]), dtype=torch.uint8).pin_memory()
+    host_in = torch.frombuffer(bytearray(band_cells), dtype=torch.uint8).pin_memory()
     e2e_times = []
     for i in range(args.steps):
         dist.barrier()

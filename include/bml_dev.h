@@ -76,10 +76,19 @@ int bml_dev_upload(bml_dev *dev, const uint8_t *src, size_t src_pitch);
 /* Copy the band's rows out, same addressing as bml_dev_upload. */
 int bml_dev_download(bml_dev *dev, uint8_t *dst, size_t dst_pitch);
 
-/* Fill the lattice exactly as the reference init_grid({n, rho, seed}) does
- * (SplitMix64 + descending Fisher–Yates), computed on the device.
- * Single-band handles only. */
+/* Fill the band's rows exactly as the reference init_grid({n, rho, seed})
+ * does (SplitMix64 + descending Fisher–Yates, src/seeding.cpp:11-51), computed
+ * on the device: parallel counter-based draws with a rejection fix-up, a
+ * stable sort of the swap targets, and chain resolution of the swaps (see
+ * csrc/bml_init.cu). n <= 65536. Needs 16·n² bytes of temporary device memory
+ * (64 GiB at n = 65536), released before returning. Connected bands call
+ * bml_dev_exchange_halos() afterwards, as after an upload. */
 int bml_dev_init_random(bml_dev *dev, double rho, uint64_t seed);
+
+/* TEST HOOK (not a reference interface): as bml_dev_init_random, but a draw r
+ * with (r & reject_mask) == 0 is rejected as well, which drives the rejection
+ * fix-up path at small n. reject_mask = 0 is exactly bml_dev_init_random. */
+int bml_dev_init_random_masked(bml_dev *dev, double rho, uint64_t seed, uint64_t reject_mask);
 
 /* One phase (step_phase). `moved` (nullable) receives the vehicles that
  * advanced (moved_in_phase). Single-band handles only. */

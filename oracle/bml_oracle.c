@@ -7,7 +7,7 @@
  * Parity pinning: tests/test_oracle.py checks every function here against the
  * reference's own known-answer vectors (SplitMix64 seed-0 sequence, the pinned
  * N=4 seed-42 lattice, FNV-1a vectors, rule truth tables, 4-torus phase cases)
- * and against tests/golden/*.json, which were produced by the UNMODIFIED
+ * and against the JSON files in tests/golden/, which were produced by the UNMODIFIED
  * reference compiled from /root/reference (oracle/_ref/ref_driver, see
  * tests/golden/make_goldens.py).
  *
@@ -53,8 +53,12 @@ int64_t orc_vehicles_per_species(int n, double rho) {
 
 /* init_grid — src/seeding.cpp:26-51. Descending Fisher-Yates over the n*n
  * interior indices; first k shuffled indices become LR, next k TB. Writes the
- * dense n*n interior into `out`. Returns 0, or 1 on invalid arguments. */
-int orc_init_grid(int n, double rho, uint64_t seed, uint8_t *out) {
+ * dense n*n interior into `out`. Returns 0, or 1 on invalid arguments.
+ * orc_init_grid_masked adds the device engine's TEST hook (include/bml_dev.h,
+ * bml_dev_init_random_masked): a draw with (r & reject_mask) == 0 is rejected
+ * as well, so tests can drive the rejection path the reference's own rule
+ * reaches less than once per 2^32 draws. reject_mask = 0 is the reference. */
+int orc_init_grid_masked(int n, double rho, uint64_t seed, uint64_t reject_mask, uint8_t *out) {
     if (n < 1 || !(rho >= 0.0 && rho <= 1.0)) return 1;
     const int64_t count = (int64_t)n * n;
     const int64_t k = orc_vehicles_per_species(n, rho);
@@ -63,7 +67,15 @@ int orc_init_grid(int n, double rho, uint64_t seed, uint8_t *out) {
     for (int64_t i = 0; i < count; ++i) cells[i] = i;
     uint64_t state = seed;
     for (int64_t i = count - 1; i > 0; --i) {
-        const int64_t j = (int64_t)orc_bounded(&state, (uint64_t)(i + 1), NULL);
+        const uint64_t m = (uint64_t)(i + 1);
+        const uint64_t rem = (UINT64_MAX % m + 1) % m; /* bounded(), src/seeding.cpp:11-19 */
+        const uint64_t top = 0 - rem;
+        uint64_t r;
+        for (;;) {
+            r = orc_splitmix64_next(&state);
+            if ((rem == 0 || r < top) && (reject_mask == 0 || (r & reject_mask) != 0)) break;
+        }
+        const int64_t j = (int64_t)(r % m);
         const int64_t t = cells[i];
         cells[i] = cells[j];
         cells[j] = t;
@@ -72,6 +84,10 @@ int orc_init_grid(int n, double rho, uint64_t seed, uint8_t *out) {
     for (int64_t i = 0; i < 2 * k; ++i) out[cells[i]] = (uint8_t)(i < k ? ORC_LR : ORC_TB);
     free(cells);
     return 0;
+}
+
+int orc_init_grid(int n, double rho, uint64_t seed, uint8_t *out) {
+    return orc_init_grid_masked(n, rho, seed, 0, out);
 }
 
 /* horizontal_rule / vertical_rule — include/bml/engine.hpp:32-42. The two

@@ -38,6 +38,7 @@
 #include <vector>
 
 #include "bml_dev.h"
+#include "bml_init.cuh"
 
 namespace {
 
@@ -1575,11 +1576,27 @@ int bml_dev_download(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
     return check_errors(d);
 }
 
-int bml_dev_init_random(bml_dev* d, double rho, uint64_t seed) {
-    (void)rho;
-    (void)seed;
+int bml_dev_init_random_masked(bml_dev* d, double rho, uint64_t seed, uint64_t reject_mask) {
     if (int rc = check(d)) return rc;
-    return fail(BML_EINVAL, "bml_dev_init_random: device-side init_grid not available in this build");
+    if (!(rho >= 0.0 && rho <= 1.0))
+        return fail(BML_EINVAL, "init_grid: density must be in [0, 1]");
+    if (static_cast<unsigned long long>(d->n) * d->n > (1ull << 32))
+        return fail(BML_EINVAL, "bml_dev_init_random: device init supports n <= 65536");
+    std::string msg;
+    const int rc = bml_init::init_planes(d->row0(d->cur), d->pitch, d->n, d->row_begin,
+                                         d->row_end, rho, seed, reject_mask, d->stream, d->sms,
+                                         &msg);
+    if (rc == 3) return fail(BML_ENOMEM, "bml_dev_init_random: " + msg);
+    if (rc != 0) return fail(BML_ECUDA, "bml_dev_init_random: " + msg);
+    if (d->single_band()) {
+        if (int r2 = fill_images(d, d->cur)) return r2;
+    }
+    BML_CUDA(cudaStreamSynchronize(d->stream));
+    return BML_OK;
+}
+
+int bml_dev_init_random(bml_dev* d, double rho, uint64_t seed) {
+    return bml_dev_init_random_masked(d, rho, seed, 0);
 }
 
 int bml_dev_counts(bml_dev* d, int64_t* lr, int64_t* tb) {

@@ -11,6 +11,7 @@
 
 #include "bml/engine.hpp"
 #include "bml/metrics.hpp"
+#include "bml/seeding.hpp"
 #include "bml_dev.h"
 
 namespace bml {
@@ -128,6 +129,21 @@ void DeviceLattice::upload(const Grid& g) {
     }
     if (bands_.size() > 1)
         for (bml_dev* h : bands_) ok(bml_dev_exchange_halos(h), "bml_dev_exchange_halos");
+}
+
+void DeviceLattice::init_random(double rho, std::uint64_t seed) {
+    for (bml_dev* h : bands_) ok(bml_dev_init_random(h, rho, seed), "bml_dev_init_random");
+    if (bands_.size() > 1)
+        for (bml_dev* h : bands_) ok(bml_dev_exchange_halos(h), "bml_dev_exchange_halos");
+}
+
+Grid init_grid_device(const SeedSpec& spec) {
+    if (spec.n < 1) throw std::invalid_argument("init_grid: n must be >= 1");
+    if (!(spec.rho >= 0.0 && spec.rho <= 1.0))
+        throw std::invalid_argument("init_grid: density must be in [0, 1]");
+    DeviceLattice lat(spec.n);
+    lat.init_random(spec.rho, spec.seed);
+    return lat.download();
 }
 
 void DeviceLattice::download(Grid& g) const {

@@ -93,6 +93,9 @@ public:
     int bands() const { return static_cast<int>(bands_.size()); }
 
     void upload(const Grid& g);
+    // The reference init_grid({n, rho, seed}) lattice, generated on the device
+    // (bit-identical; bml_dev_init_random). n <= 65536.
+    void init_random(double rho, std::uint64_t seed);
     void download(Grid& g) const;  // writes the interior of g (any layout, size n)
     Grid download() const;         // halo-layout grid, ghosts unfilled
 
@@ -117,5 +120,10 @@ private:
     std::vector<bml_dev*> bands_;
     int block_steps_ = 8;
 };
+
+struct SeedSpec;
+// init_grid (seeding.hpp) computed on the GPU and read back: same Grid, bit for
+// bit, without the serial host shuffle (minutes at n = 65536). n <= 65536.
+Grid init_grid_device(const SeedSpec& spec);
 
 }  // namespace bml

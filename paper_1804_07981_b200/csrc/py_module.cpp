@@ -146,11 +146,13 @@ PYBIND11_MODULE(_bml, m) {
         });
 
     m.def("init_grid",
-          [](int n, double rho, std::uint64_t seed) {
+          [](int n, double rho, std::uint64_t seed, bool on_device) {
               py::gil_scoped_release nogil;
+              if (on_device) return bml::init_grid_device({n, rho, seed});
               return bml::init_grid({n, rho, seed});
           },
-          py::arg("n"), py::arg("rho"), py::arg("seed"));
+          py::arg("n"), py::arg("rho"), py::arg("seed"), py::arg("on_device") = false,
+          "The reference init_grid lattice; on_device=True computes the same lattice on the GPU.");
 
     m.def("vehicles_per_species", &bml::vehicles_per_species, py::arg("n"), py::arg("rho"));
 
@@ -199,6 +201,8 @@ PYBIND11_MODULE(_bml, m) {
         .def_property_readonly("n", &bml::DeviceLattice::n)
         .def_property_readonly("bands", &bml::DeviceLattice::bands)
         .def("upload", &bml::DeviceLattice::upload, py::arg("grid"),
+             py::call_guard<py::gil_scoped_release>())
+        .def("init_random", &bml::DeviceLattice::init_random, py::arg("rho"), py::arg("seed"),
              py::call_guard<py::gil_scoped_release>())
         .def("download", py::overload_cast<>(&bml::DeviceLattice::download, py::const_),
              py::call_guard<py::gil_scoped_release>())

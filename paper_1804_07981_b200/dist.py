@@ -74,6 +74,7 @@ class _Abi:
         lib.bml_dev_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_size_t)]
         lib.bml_dev_connect.argtypes = [vp, vp, vp]
         lib.bml_dev_exchange_halos.argtypes = [vp]
+        lib.bml_dev_init_random.argtypes = [vp, ctypes.c_double, ctypes.c_uint64]
         lib.bml_dev_sync.argtypes = [vp]
         lib.bml_dev_set_stream.argtypes = [vp, vp]
         lib.bml_dev_configure.argtypes = [vp, ctypes.c_int, ctypes.c_int]
@@ -127,6 +128,11 @@ class BandLattice:
             self._keep = buf
             ptr = ctypes.addressof(buf)
         self.abi.check(self.abi.lib.bml_dev_upload(self.h, ctypes.c_void_p(ptr), pitch), "upload")
+
+    def init_random(self, rho, seed):
+        """This band's rows of the reference init_grid({n, rho, seed}) lattice,
+        generated on the device (bml_dev_init_random); call exchange_halos() next."""
+        self.abi.check(self.abi.lib.bml_dev_init_random(self.h, rho, seed), "init_random")
 
     def exchange_halos(self):
         self.abi.check(self.abi.lib.bml_dev_exchange_halos(self.h), "exchange_halos")

@@ -40,6 +40,8 @@ class Oracle:
         lib.orc_vehicles_per_species.argtypes = [ctypes.c_int, ctypes.c_double]
         lib.orc_vehicles_per_species.restype = ctypes.c_int64
         lib.orc_init_grid.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_uint64, ctypes.c_char_p]
+        lib.orc_init_grid_masked.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
+                                             ctypes.c_uint64, ctypes.c_char_p]
         lib.orc_phase.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int]
         lib.orc_moved.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int]
         lib.orc_moved.restype = ctypes.c_int64
@@ -64,6 +66,11 @@ class Oracle:
     def init_grid(self, n, rho, seed):
         buf = ctypes.create_string_buffer(n * n)
         assert self.lib.orc_init_grid(n, rho, seed, buf) == 0
+        return buf.raw[: n * n]
+
+    def init_grid_masked(self, n, rho, seed, reject_mask):
+        buf = ctypes.create_string_buffer(n * n)
+        assert self.lib.orc_init_grid_masked(n, rho, seed, reject_mask, buf) == 0
         return buf.raw[: n * n]
 
     def phase(self, n, cells, phase):
