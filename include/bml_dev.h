@@ -26,6 +26,8 @@
  *                         and the loops of Grid run(...)                   src/engine.cpp:206-235
  *                         with moved_in_phase / count_vehicles fused       src/metrics.cpp:8-29
  *   bml_dev_counts        VehicleCounts count_vehicles(const Grid&)        include/bml/metrics.hpp:20
+ *   bml_dev_digest        std::uint64_t grid_digest(const Grid&)           include/bml/digest.hpp:23
+ *   bml_dev_encode_ppm    std::vector<uint8_t> encode_ppm(const Grid&)     include/bml/snapshot.hpp:21
  *   bml_dev_download      readback: Grid::interior / data                  include/bml/grid.hpp:38-47
  *   bml_dev_destroy       ~GridPair
  *
@@ -103,6 +105,21 @@ int bml_dev_phase(bml_dev *dev, int phase, int64_t *moved);
 int bml_dev_step(bml_dev *dev, int64_t steps, int64_t *lr_moved, int64_t *tb_moved,
                  int64_t *lr_count, int64_t *tb_count);
 
+/* grid_digest (FNV-1a-64 over the cells, row-major; src/digest.cpp:5-14),
+ * computed on the device, bit-identical. Single-band handles only. */
+int bml_dev_digest(bml_dev *dev, uint64_t *digest);
+
+/* The band's rows as a digest segment (6 words: p^cells, B[4], packed low-bit
+ * map; see csrc/bml_digest.cu). bml_digest_finish() combines the segments of
+ * consecutive bands (in row order) into grid_digest. Host arithmetic only. */
+int bml_dev_digest_segment(bml_dev *dev, uint64_t seg[6]);
+int bml_digest_finish(const uint64_t *segs, int count, uint64_t *digest);
+
+/* The band's rows as binary-PPM pixels (3 bytes per cell, encode_ppm's body
+ * without the "P6\n<n> <n>\n255\n" header; src/snapshot.cpp:21-36), written
+ * to `dst` (host or device memory), rows `dst_pitch` bytes apart. */
+int bml_dev_encode_ppm(bml_dev *dev, uint8_t *dst, size_t dst_pitch);
+
 /* Vehicle counts of the band's rows (count_vehicles). */
 int bml_dev_counts(bml_dev *dev, int64_t *lr, int64_t *tb);
 
@@ -114,7 +131,9 @@ int bml_dev_sync(bml_dev *dev);
 
 /* Tuning knobs (0 = keep current): temporal block depth (full steps fused per
  * launch / ghost depth of the resident kernel, 1..16, default 16) and rows per
- * warp strip of the streaming kernel (1..1000, -1 = automatic, the default). */
+ * warp strip of the streaming kernel (1..65536, -1 = automatic, the default;
+ * rows are split evenly over rows / strip_rows strips; -ns with ns >= 2 asks
+ * for exactly ns strips). */
 int bml_dev_configure(bml_dev *dev, int block_steps, int strip_rows);
 
 /* Small lattices (n % 32 == 0, n <= 1024) run the whole step loop in one
@@ -124,6 +143,10 @@ int bml_dev_configure(bml_dev *dev, int block_steps, int strip_rows);
  * last bml_dev_step (0 = streaming kernel). */
 int bml_dev_set_resident(bml_dev *dev, int mode);
 int bml_dev_path(bml_dev *dev, int *resident_cluster);
+
+/* Geometry of the last streaming-kernel launch: row strips, work items
+ * (strips x warp columns) and CTAs. */
+int bml_dev_last_launch(bml_dev *dev, int *nstrips, int *items, int *grid);
 
 /* Kernel statistics since the last reset: launches of the step kernels and
  * their summed device time (CUDA events around each launch; enable first). */

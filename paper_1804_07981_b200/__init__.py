@@ -24,11 +24,13 @@ try:
         Phase,
         Regime,
         StepMetrics,
+        VerifyReport,
         __version__,
         backend_from_name,
         classify,
         count_vehicles,
         device_count,
+        encode_ppm,
         init_grid,
         lane_width,
         library_version,
@@ -37,6 +39,8 @@ try:
         step,
         step_phase,
         vehicles_per_species,
+        verify_backends,
+        write_ppm,
     )
 except ImportError as exc:  # pragma: no cover - exercised only on broken installs
     raise ImportError(
@@ -54,11 +58,13 @@ __all__ = [
     "Phase",
     "Regime",
     "StepMetrics",
+    "VerifyReport",
     "__version__",
     "backend_from_name",
     "classify",
     "count_vehicles",
     "device_count",
+    "encode_ppm",
     "init_grid",
     "lane_width",
     "library_version",
@@ -67,5 +73,7 @@ __all__ = [
     "step",
     "step_phase",
     "vehicles_per_species",
+    "verify_backends",
+    "write_ppm",
     "LIB_DEV",
 ]

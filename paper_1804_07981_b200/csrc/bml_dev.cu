@@ -35,9 +35,11 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "bml_dev.h"
+#include "bml_digest.cuh"
 #include "bml_init.cuh"
 
 namespace {
@@ -49,6 +51,12 @@ constexpr unsigned kFull = 0xffffffffu;
 
 #ifndef BML_FMA_SHIFTS
 #define BML_FMA_SHIFTS 0
+#endif
+#ifndef BML_STEP_MIN_CTAS
+#define BML_STEP_MIN_CTAS 3
+#endif
+#ifndef BML_IMAD_OR
+#define BML_IMAD_OR 1
 #endif
 #ifndef BML_RES_SKIP
 #define BML_RES_SKIP 0
@@ -84,7 +92,7 @@ struct StepArgs {
     int W;             // words per row
     int pitch;         // words between rows
     int rows;          // rows in this band
-    int strip_rows;    // rows per warp strip (the last strip also takes the remainder)
+    int strip_rows;    // unused by the kernel (rows are split evenly over nstrips)
     int nstrips;
     int ncols;         // warp columns per strip
     int items;         // nstrips * ncols
@@ -102,6 +110,8 @@ struct StepArgs {
     int step_base;
     int* error_flag;
     uint32_t two, half;  // 2 and 2^31, passed at run time so ptxas keeps IMAD (FMA pipe) shifts
+    uint32_t one;        // 1, at run time: IMAD-issued ORs of disjoint planes (BML_IMAD_OR)
+    int sms;             // SM count (CTA wave of blockIdx, for the warp-slot rotation)
 };
 
 // --------------------------------------------------------------- device utils
@@ -166,9 +176,20 @@ __device__ __forceinline__ uint2 load_cells(const uint2* row, int word, int c0, 
 
 __device__ __forceinline__ void put(uint2* p, uint32_t l, uint32_t t) { *p = make_uint2(l, t); }
 
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 // Asynchronous 8-byte global->shared copies (LDGSTS) feeding a per-warp ring of
 // input rows, so each warp keeps kRing-1 rows of loads in flight.
-constexpr int kRing = 8;
+#ifndef BML_RING
+#define BML_RING 6
+#endif
+// BML_RING == 6 (the main loop's unroll factor) makes every slot index a
+// compile-time constant; 8 keeps one more row in flight with computed slots.
+constexpr int kRing = BML_RING;
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
@@ -211,6 +232,7 @@ struct PipeState {
 struct StripCtx {
     int lane, r_lo, r_hi, out_word;
     uint32_t valid;
+    unsigned span;  // rows this lane stores (r_hi - r_lo, or 0 for ghost lanes)
 };
 
 // Final-stage output of row o: the row itself plus its ghost images (the
@@ -221,11 +243,22 @@ struct StripCtx {
 template <int MODE>
 __device__ __forceinline__ void store_row(const StepArgs& a, const StripCtx& c, int o, uint32_t l,
                                           uint32_t t) {
-    const bool row_ok = o >= c.r_lo && o < c.r_hi;
-    const bool st = row_ok && c.valid != 0u;
+    const bool st = static_cast<unsigned>(o - c.r_lo) < c.span;
     const uint2 v = make_uint2(l & c.valid, t & c.valid);
+    if (MODE != kGeneric) {
+        const long long off = static_cast<long long>(o) * a.pitch + c.out_word;
+        if (st) a.dst[off] = v;
+        {
+            uint2* top_img = a.single_band ? a.dst + static_cast<long long>(a.rows) * a.pitch : a.up_halo;
+            uint2* bot_img = a.single_band ? a.dst - static_cast<long long>(a.rows) * a.pitch
+                                           : a.down_halo - static_cast<long long>(a.rows) * a.pitch;
+            if (st && o < kHalo) top_img[off] = v;            // row o -> ghost row rows+o (or up peer)
+            if (st && o >= a.rows - kHalo) bot_img[off] = v;  // row o -> ghost row o-rows (or down peer)
+        }
+        return;
+    }
     const long long off = static_cast<long long>(o) * a.pitch + c.out_word;
-    if (MODE == kGeneric) {
+    {
         if (st) {
             a.dst[off] = v;
             if (a.single_band) {
@@ -238,14 +271,7 @@ __device__ __forceinline__ void store_row(const StepArgs& a, const StripCtx& c, 
                 if (o >= a.rows - kHalo) a.down_halo[off - static_cast<long long>(a.rows) * a.pitch] = v;
             }
         }
-        return;
     }
-    if (st) a.dst[off] = v;
-    uint2* top_img = a.single_band ? a.dst + static_cast<long long>(a.rows) * a.pitch : a.up_halo;
-    uint2* bot_img = a.single_band ? a.dst - static_cast<long long>(a.rows) * a.pitch
-                                   : a.down_halo - static_cast<long long>(a.rows) * a.pitch;
-    if (st && o < kHalo) top_img[off] = v;            // row o -> ghost row rows+o (or up peer)
-    if (st && o >= a.rows - kHalo) bot_img[off] = v;  // row o -> ghost row o-rows (or down peer)
 }
 
 template <int K, int MODE, bool COUNT, int P>
@@ -260,7 +286,14 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
         const uint32_t tB = (s == 0) ? q.xt[(P3 + 2) % 3] : q.nt[s > 0 ? s - 1 : 0][(P3 + 1) % 3];
         const uint32_t tA = (s == 0) ? q.xt[(P3 + 1) % 3] : q.nt[s > 0 ? s - 1 : 0][P3];
         // ---- LR phase on row rho = j - 2s
+#if BML_IMAD_OR
+        // L and T are disjoint planes (a cell holds one vehicle), so L | T ==
+        // L + T: issue it as IMAD on the FMA pipe (runtime multiplier 1 keeps
+        // ptxas from folding it back into an ALU LOP3/IADD3).
+        const uint32_t O = imad(L, a.one, T);
+#else
         const uint32_t O = L | T;
+#endif
 #if BML_FMA_SHIFTS
         // shifts on the FMA pipe (IMAD / IMAD.HI); the ALU pipe is the bottleneck
         const uint32_t lc = __umulhi(L, a.two);   // L >> 31: carry into the right neighbour
@@ -288,7 +321,11 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
         const uint32_t nextO = __funnelshift_r(O, Or, 1);
 #endif
         const uint32_t Lp = (prevL & ~O) | (L & nextO);
+#if BML_IMAD_OR
+        const uint32_t Op = imad(Lp, a.one, T);  // Lp, T disjoint after the LR phase
+#else
         const uint32_t Op = Lp | T;
+#endif
         // ---- TB phase emits row rho - 1
         const uint32_t newT = (tA & ~q.oc[s]) | (tB & Op);
         const uint32_t newL = q.lp[s][(P2 + 1) % 2];
@@ -313,21 +350,26 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
 }
 
 template <int K, int MODE, bool COUNT>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, BML_STEP_MIN_CTAS)
 step_block_kernel(const StepArgs a) {
     const int lane = threadIdx.x & 31;
     const int warps_total = gridDim.x * kWarpsPerCta;
     __shared__ uint2 ring[kWarpsPerCta][kRing][32];
     uint2 (*my_ring)[32] = ring[threadIdx.x >> 5];
 
-    for (int item = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5); item < a.items;
-         item += warps_total) {
+    // Warp-major item order: items 0..grid-1 go to one warp of every CTA, so
+    // when there are fewer items than warps they spread evenly over the SMs.
+    // The warp slot rotates with the CTA's wave (blockIdx / SMs), so the CTAs
+    // sharing an SM put their first busy warps on different SM sub-partitions.
+    const int slot = ((threadIdx.x >> 5) + blockIdx.x / a.sms) % kWarpsPerCta;
+    for (int item = slot * gridDim.x + blockIdx.x; item < a.items; item += warps_total) {
         const int strip = item / a.ncols;
         const int col = item - strip * a.ncols;
         StripCtx c;
         c.lane = lane;
-        c.r_lo = strip * a.strip_rows;
-        c.r_hi = (strip == a.nstrips - 1) ? a.rows : c.r_lo + a.strip_rows;
+        // rows split evenly: strip i owns [i*rows/nstrips, (i+1)*rows/nstrips)
+        c.r_lo = static_cast<int>(static_cast<long long>(strip) * a.rows / a.nstrips);
+        c.r_hi = static_cast<int>(static_cast<long long>(strip + 1) * a.rows / a.nstrips);
 
         int word = lane, c0 = 0;
         c.out_word = lane;
@@ -342,6 +384,8 @@ step_block_kernel(const StepArgs a) {
             if (cc < 0) cc += a.n;
             c0 = static_cast<int>(cc);
         }
+
+        c.span = c.valid ? static_cast<unsigned>(c.r_hi - c.r_lo) : 0u;
 
         if (!a.single_band) {
             if (c.r_lo == 0) wait_flag(a.top_flag, a.expect, a.error_flag);
@@ -370,26 +414,32 @@ step_block_kernel(const StepArgs a) {
             const uint2* row = a.src + static_cast<long long>(j) * a.pitch;
             return load_cells<MODE>(row, word, c0, a.n, coherent && (j < 0 || j >= a.rows));
         };
-        // cp.async ring: row j lands in slot (j - j_begin) % kRing
+        // cp.async ring: row j lands in slot (j - j_begin) % kRing; kRing == the
+        // unroll factor, so every slot index below is a compile-time constant
         const uint2* gsrc = a.src + static_cast<long long>(j_begin) * a.pitch + word;
         int j_issue = j_begin;
-        auto issue_next = [&]() {
-            if (j_issue < j_load_end)
-                cp_async8(&my_ring[(j_issue - j_begin) & (kRing - 1)][lane], gsrc);
+        auto issue_to = [&](int slot_idx) {
+            if (j_issue < j_load_end) cp_async8(&my_ring[slot_idx][lane], gsrc);
             cp_async_commit();
             ++j_issue;
             gsrc += a.pitch;
         };
-        auto next_row = [&](int j, uint2& nx0, uint2& nx1) -> uint2 {
+        auto next_row = [&](auto p_const, uint2& nx0, uint2& nx1) -> uint2 {
+            constexpr int P = decltype(p_const)::value;
             uint2 x;
             if (MODE == kGeneric) {
                 x = nx0;
                 nx0 = nx1;
-                nx1 = fetch(j + 2);
+                nx1 = fetch(j_issue);
+                ++j_issue;
+            } else if (kRing == 6) {
+                cp_async_wait<kRing - 2>();
+                x = my_ring[P][lane];
+                issue_to((P + kRing - 1) % kRing);
             } else {
                 cp_async_wait<kRing - 2>();
-                x = my_ring[(j - j_begin) & (kRing - 1)][lane];
-                issue_next();
+                x = my_ring[(j_issue - (kRing - 1) - j_begin) & (kRing - 1)][lane];
+                issue_to((j_issue - j_begin) & (kRing - 1));
             }
             return x;
         };
@@ -398,18 +448,25 @@ step_block_kernel(const StepArgs a) {
         if (MODE == kGeneric) {
             nx0 = fetch(j_begin);
             nx1 = fetch(j_begin + 1);
+            j_issue = j_begin + 2;
         } else {
             __syncwarp();
 #pragma unroll
-            for (int i = 0; i < kRing - 1; ++i) issue_next();
+            for (int i = 0; i < kRing - 1; ++i) issue_to(i);
         }
+        using P0 = std::integral_constant<int, 0>;
+        using P1 = std::integral_constant<int, 1>;
+        using P2 = std::integral_constant<int, 2>;
+        using P3 = std::integral_constant<int, 3>;
+        using P4 = std::integral_constant<int, 4>;
+        using P5 = std::integral_constant<int, 5>;
         for (int j = j_begin; j < j_end; j += 6) {
-            pipe_iter<K, MODE, COUNT, 0>(q, next_row(j, nx0, nx1), j, a, c);
-            pipe_iter<K, MODE, COUNT, 1>(q, next_row(j + 1, nx0, nx1), j + 1, a, c);
-            pipe_iter<K, MODE, COUNT, 2>(q, next_row(j + 2, nx0, nx1), j + 2, a, c);
-            pipe_iter<K, MODE, COUNT, 3>(q, next_row(j + 3, nx0, nx1), j + 3, a, c);
-            pipe_iter<K, MODE, COUNT, 4>(q, next_row(j + 4, nx0, nx1), j + 4, a, c);
-            pipe_iter<K, MODE, COUNT, 5>(q, next_row(j + 5, nx0, nx1), j + 5, a, c);
+            pipe_iter<K, MODE, COUNT, 0>(q, next_row(P0{}, nx0, nx1), j, a, c);
+            pipe_iter<K, MODE, COUNT, 1>(q, next_row(P1{}, nx0, nx1), j + 1, a, c);
+            pipe_iter<K, MODE, COUNT, 2>(q, next_row(P2{}, nx0, nx1), j + 2, a, c);
+            pipe_iter<K, MODE, COUNT, 3>(q, next_row(P3{}, nx0, nx1), j + 3, a, c);
+            pipe_iter<K, MODE, COUNT, 4>(q, next_row(P4{}, nx0, nx1), j + 4, a, c);
+            pipe_iter<K, MODE, COUNT, 5>(q, next_row(P5{}, nx0, nx1), j + 5, a, c);
             if (!a.single_band) {
                 // rows j-2K+1 .. j-2K+6 were just stored
                 const int o_last = j - 2 * K + 6;
@@ -938,6 +995,25 @@ __global__ void unpack_kernel(const uint2* __restrict__ src, uint8_t* bytes, lon
     }
 }
 
+// Bit planes -> binary-PPM pixels (snapshot.cpp:21-36, snapshot.hpp kLrColor /
+// kTbColor / kEmptyColor): LR (255,0,0), TB (0,0,255), empty (255,255,255), so
+// R = ~T, G = empty, B = ~L per cell. One thread per 32-cell word.
+__global__ void ppm_kernel(const uint2* __restrict__ src, uint8_t* rgb, long long rpitch, int n,
+                           int W, int pitch, int rows) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long long>(rows) * W) return;
+    const int r = static_cast<int>(idx / W), w = static_cast<int>(idx % W);
+    const uint2 x = src[static_cast<long long>(r) * pitch + w];
+    uint8_t* p = rgb + r * rpitch + 96LL * w;
+    const int cells = min(32, n - 32 * w);
+    for (int i = 0; i < cells; ++i) {
+        const uint32_t l = (x.x >> i) & 1u, t = (x.y >> i) & 1u;
+        p[3 * i + 0] = t ? 0 : 255;
+        p[3 * i + 1] = (l | t) ? 0 : 255;
+        p[3 * i + 2] = l ? 0 : 255;
+    }
+}
+
 // Ghost rows of a single band: row h in [-kHalo,0) U [rows, rows+kHalo) is
 // the image of row (h mod n).
 __global__ void fill_images_kernel(uint2* buf, int n, int W, int pitch, int rows) {
@@ -1039,9 +1115,10 @@ struct bml_dev {
     uint32_t last_mask = kFull;
     int mode = kGeneric;
     int block_steps = 16;
-    int strip_rows = 0;      // 0 = auto (auto_strip_rows)
+    int strip_rows = 0;      // 0 = auto (choose_nstrips); < 0: exactly -strip_rows strips
     int resident = 1;        // 1: use the cluster-resident kernel when the lattice qualifies
     int resident_cluster = 0;  // cluster size actually used by the last resident launch
+    int last_nstrips = 0, last_grid = 0, last_items = 0;  // last streaming launch
     int sms = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
@@ -1195,26 +1272,40 @@ int check_errors(bml_dev* d) {
     return BML_OK;
 }
 
-// Rows per warp strip. A strip of R rows costs R + 3K - 1 pipeline iterations
-// (2K ghost rows + K-1 drain), so long strips waste less; but an SM needs about
-// four warps to keep its ALU pipes saturated. Model: time ~ (R + 3K) *
-// max(ceil(items / SMs), 4), R a power of two in [16, 256]. It reproduces the
-// measured optima on B200 (profiles/r1_abi_sweep_v3.jsonl): n=8192 -> 128,
-// n=32768 -> 256.
-int auto_strip_rows(const bml_dev* d, int k) {
-    if (d->strip_rows > 0) return d->strip_rows;
+// Strips per launch. A strip of R rows costs R + 3K - 1 pipeline iterations
+// of K stages (2K ghost rows + K-1 drain). Items (strips x warp columns) are
+// spread evenly over the SMs and their four sub-partitions (SMSPs; warp-major
+// order with slot rotation, see step_block_kernel). Per-SMSP time model, in
+// clocks for one pipeline iteration of each of its u warps at K = 16, measured
+// on B200 (profiles/r1_sweep_strips*.jsonl, ncu issue statistics): u = 1: 460
+// (one warp's K independent stage chains cannot fill the issue slots), u = 2:
+// 774, u = 3: 1050 (~350 per warp: the ALU pipe and issue slots saturate).
+// An SM runs ceil(items / SMs) warps' items in rounds of at most
+// warps_per_sm. Rows are split evenly over the strips.
+long long smsp_round_cost(long long w) {
+    const long long u = (w + 3) / 4;
+    if (u <= 1) return 460;
+    if (u == 2) return 774;
+    return 1050 + (u - 3) * 350;
+}
+
+int choose_nstrips(const bml_dev* d, int k, int warps_per_sm) {
+    const int min_rows = d->connected ? kHalo : 1;
+    if (d->strip_rows > 0) return std::max(1, d->rows / std::max(d->strip_rows, min_rows));
+    if (d->strip_rows < 0) return std::max(1, std::min(-d->strip_rows, d->rows / min_rows));
     const long long cols = d->ncols();
+    const int max_strips = std::max(1, d->rows / min_rows);
     long long best_cost = -1;
-    int best = 16;
-    for (int r = 16; r <= 256; r *= 2) {
-        if (d->connected && r < kHalo) continue;
-        const long long strips = std::max(1, d->rows / r);
-        const long long items = strips * cols;
-        const long long per_sm = (items + d->sms - 1) / d->sms;
-        const long long cost = static_cast<long long>(std::min(r, d->rows) + 3 * k) * std::max(per_sm, 4LL);
-        if (best_cost < 0 || cost <= best_cost) {
+    int best = 1;
+    for (int ns = 1; ns <= max_strips; ++ns) {
+        const long long r = (d->rows + ns - 1) / ns;
+        const long long per_sm = (ns * cols + d->sms - 1) / d->sms;
+        const long long full = per_sm / warps_per_sm, last = per_sm % warps_per_sm;
+        const long long cost = (r + 3 * k) * (full * smsp_round_cost(warps_per_sm) +
+                                              (last ? smsp_round_cost(last) : 0));
+        if (best_cost < 0 || cost < best_cost) {
             best_cost = cost;
-            best = r;
+            best = ns;
         }
     }
     return best;
@@ -1223,10 +1314,13 @@ int auto_strip_rows(const bml_dev* d, int k) {
 int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_stride) {
     StepKernel kern = pick(k, d->mode, count);
     if (!kern) return fail(BML_EINVAL, "unsupported block depth " + std::to_string(k));
-    const int strip = auto_strip_rows(d, k);
-    // floor: every strip has >= strip_rows rows (the last absorbs the
-    // remainder), so the ghost-row sources of a band never straddle strips
-    const int nstrips = std::max(1, d->rows / strip);
+    int max_ctas_per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_ctas_per_sm, kern, kWarpsPerCta * 32, 0);
+    max_ctas_per_sm = std::max(1, max_ctas_per_sm);
+    // every strip has >= min(strip_rows, 16) rows, so for connected bands the
+    // ghost-row sources of a band never straddle strips
+    const int nstrips = choose_nstrips(d, k, max_ctas_per_sm * kWarpsPerCta);
+    const int strip = d->rows / nstrips;
     StepArgs a{};
     a.src = d->row0(d->cur);
     a.dst = d->row0(d->cur ^ 1);
@@ -1254,12 +1348,17 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
     a.error_flag = d->err + 1;
     a.two = 2u;
     a.half = 0x80000000u;
+    a.one = 1u;
+    a.sms = d->sms;
 
-    int max_ctas_per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_ctas_per_sm, kern, kWarpsPerCta * 32, 0);
-    max_ctas_per_sm = std::max(1, max_ctas_per_sm);
-    const int want = (a.items + kWarpsPerCta - 1) / kWarpsPerCta;
-    const int grid = std::max(1, std::min(want, d->sms * max_ctas_per_sm));
+    // sms x m CTAs: every SM gets the same number of CTAs, the warp-major item
+    // order then spreads the items evenly over the SMs
+    const int m = std::min(max_ctas_per_sm,
+                           std::max(1, (a.items + d->sms * kWarpsPerCta - 1) / (d->sms * kWarpsPerCta)));
+    const int grid = std::max(1, std::min(d->sms * m, a.items));
+    d->last_nstrips = nstrips;
+    d->last_grid = grid;
+    d->last_items = a.items;
 
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (d->timing) {
@@ -1483,8 +1582,8 @@ int bml_dev_configure(bml_dev* d, int block_steps, int strip_rows) {
         d->block_steps = block_steps;
     }
     if (strip_rows) {
-        if (strip_rows < -1 || strip_rows > 1000)
-            return fail(BML_EINVAL, "strip_rows must be in [1, 1000] (or -1 for auto)");
+        if (strip_rows < -65536 || strip_rows > 65536)
+            return fail(BML_EINVAL, "strip_rows must be in [1, 65536], -1 (auto) or -ns (ns >= 2 strips)");
         if (strip_rows == -1) strip_rows = 0;
         if (d->connected && strip_rows > 0 && strip_rows < kHalo)
             return fail(BML_EINVAL, "connected bands need strip_rows >= 16");
@@ -1503,6 +1602,14 @@ int bml_dev_set_resident(bml_dev* d, int mode) {
 int bml_dev_path(bml_dev* d, int* resident_cluster) {
     if (!d) return fail(BML_EINVAL, "null bml_dev handle");
     if (resident_cluster) *resident_cluster = d->resident_cluster;
+    return BML_OK;
+}
+
+int bml_dev_last_launch(bml_dev* d, int* nstrips, int* items, int* grid) {
+    if (!d) return fail(BML_EINVAL, "null bml_dev handle");
+    if (nstrips) *nstrips = d->last_nstrips;
+    if (items) *items = d->last_items;
+    if (grid) *grid = d->last_grid;
     return BML_OK;
 }
 
@@ -1597,6 +1704,56 @@ int bml_dev_init_random_masked(bml_dev* d, double rho, uint64_t seed, uint64_t r
 
 int bml_dev_init_random(bml_dev* d, double rho, uint64_t seed) {
     return bml_dev_init_random_masked(d, rho, seed, 0);
+}
+
+int bml_dev_encode_ppm(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
+    if (int rc = check(d)) return rc;
+    if (!dst) return fail(BML_EINVAL, "bml_dev_encode_ppm: dst is null");
+    const size_t row_bytes = 3 * static_cast<size_t>(d->n);
+    if (dst_pitch < row_bytes) return fail(BML_EINVAL, "bml_dev_encode_ppm: pitch smaller than a row");
+    uint8_t* rgb = nullptr;
+    BML_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rgb), row_bytes * d->rows, d->stream));
+    const long long total = static_cast<long long>(d->rows) * d->W;
+    ppm_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, d->stream>>>(
+        d->row0(d->cur), rgb, static_cast<long long>(row_bytes), d->n, d->W, d->pitch, d->rows);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(dst, dst_pitch, rgb, row_bytes, row_bytes, d->rows, cudaMemcpyDefault,
+                              d->stream);
+    cudaFreeAsync(rgb, d->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "bml_dev_encode_ppm");
+    return BML_OK;
+}
+
+int bml_dev_digest_segment(bml_dev* d, uint64_t seg[6]) {
+    if (int rc = check(d)) return rc;
+    if (!seg) return fail(BML_EINVAL, "bml_dev_digest_segment: seg is null");
+    std::string msg;
+    const int rc = bml_digest::segment(d->row0(d->cur), d->n, d->W, d->pitch, d->rows, d->stream,
+                                       d->sms, seg, &msg);
+    if (rc == 3) return fail(BML_ENOMEM, msg);
+    if (rc != 0) return fail(BML_ECUDA, msg);
+    return BML_OK;
+}
+
+int bml_dev_digest(bml_dev* d, uint64_t* digest) {
+    if (int rc = check(d)) return rc;
+    if (!digest) return fail(BML_EINVAL, "bml_dev_digest: digest is null");
+    if (!d->single_band())
+        return fail(BML_EINVAL, "bml_dev_digest: a row band hashes only its rows; combine "
+                                "bml_dev_digest_segment() of all bands with bml_digest_finish()");
+    uint64_t seg[6];
+    if (int rc = bml_dev_digest_segment(d, seg)) return rc;
+    *digest = bml_digest::finish(seg, 1);
+    return BML_OK;
+}
+
+int bml_digest_finish(const uint64_t* segs, int count, uint64_t* digest) {
+    if (!digest || count < 0 || (count > 0 && !segs))
+        return fail(BML_EINVAL, "bml_digest_finish: bad arguments");
+    *digest = bml_digest::finish(segs, count);
+    return BML_OK;
 }
 
 int bml_dev_counts(bml_dev* d, int64_t* lr, int64_t* tb) {

@@ -8,10 +8,12 @@
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <vector>
 
 #include "bml/engine.hpp"
 #include "bml/metrics.hpp"
 #include "bml/seeding.hpp"
+#include "bml/snapshot.hpp"
 #include "bml_dev.h"
 
 namespace bml {
@@ -144,6 +146,29 @@ Grid init_grid_device(const SeedSpec& spec) {
     DeviceLattice lat(spec.n);
     lat.init_random(spec.rho, spec.seed);
     return lat.download();
+}
+
+std::vector<std::uint8_t> DeviceLattice::encode_ppm() const {
+    const std::string header = ppm_header(n_);
+    std::vector<std::uint8_t> out(header.size() + 3u * static_cast<std::size_t>(n_) * n_);
+    std::copy(header.begin(), header.end(), out.begin());
+    for (bml_dev* h : bands_) {
+        int r0 = 0;
+        ok(bml_dev_info(h, nullptr, &r0, nullptr, nullptr, nullptr, nullptr), "bml_dev_info");
+        ok(bml_dev_encode_ppm(h, out.data() + header.size() + 3u * static_cast<std::size_t>(r0) * n_,
+                              3u * static_cast<std::size_t>(n_)),
+           "bml_dev_encode_ppm");
+    }
+    return out;
+}
+
+std::uint64_t DeviceLattice::digest() const {
+    std::vector<std::uint64_t> segs(6 * bands_.size());
+    for (std::size_t b = 0; b < bands_.size(); ++b)
+        ok(bml_dev_digest_segment(bands_[b], segs.data() + 6 * b), "bml_dev_digest_segment");
+    std::uint64_t h = 0;
+    ok(bml_digest_finish(segs.data(), static_cast<int>(bands_.size()), &h), "bml_digest_finish");
+    return h;
 }
 
 void DeviceLattice::download(Grid& g) const {

@@ -105,6 +105,10 @@ public:
     std::vector<StepMetrics> step_with_metrics(long steps, long first_step = 1);
     std::int64_t phase(Phase p);  // returns moved_in_phase
     VehicleCounts counts() const;
+    // grid_digest (digest.hpp) of the device lattice, computed on the GPU(s).
+    std::uint64_t digest() const;
+    // encode_ppm (snapshot.hpp) of the device lattice; pixels expanded on the GPU.
+    std::vector<std::uint8_t> encode_ppm() const;
 
     void configure(int block_steps, int strip_rows);
     // Small-lattice cluster-resident kernel: enabled by default; resident_cluster()

@@ -16,6 +16,8 @@
 #include "bml/engine.hpp"
 #include "bml/metrics.hpp"
 #include "bml/seeding.hpp"
+#include "bml/snapshot.hpp"
+#include "bml/verify.hpp"
 #include "bml_dev.h"
 
 namespace py = pybind11;
@@ -154,6 +156,43 @@ PYBIND11_MODULE(_bml, m) {
           py::arg("n"), py::arg("rho"), py::arg("seed"), py::arg("on_device") = false,
           "The reference init_grid lattice; on_device=True computes the same lattice on the GPU.");
 
+    py::class_<bml::VerifyReport>(m, "VerifyReport")
+        .def_property_readonly("ok", &bml::VerifyReport::ok)
+        .def_readonly("conserved", &bml::VerifyReport::conserved)
+        .def_property_readonly("digests", [](const bml::VerifyReport& r) {
+            py::dict out;
+            for (const auto& d : r.digests) out[py::str(d.path)] = d.digest;
+            return out;
+        })
+        .def_property_readonly("mismatch", [](const bml::VerifyReport& r) -> py::object {
+            if (!r.mismatch) return py::none();
+            return py::make_tuple(r.mismatch->a, r.mismatch->b, r.mismatch->row, r.mismatch->col);
+        });
+
+    m.def("verify_backends",
+          [](int n, double rho, long steps, std::uint64_t seed, int threads) {
+              bml::SimConfig cfg;
+              cfg.n = n;
+              cfg.rho = rho;
+              cfg.steps = steps;
+              cfg.seed = seed;
+              cfg.threads = 1;
+              (void)threads;  // reference signature; the device paths take no thread count
+              cfg.backend = bml::Backend::B200;
+              py::gil_scoped_release nogil;
+              return bml::verify_backends(cfg);
+          },
+          py::arg("n"), py::arg("rho"), py::arg("steps"), py::arg("seed") = 1,
+          py::arg("threads") = 1,
+          "Run the four device code paths from one initial grid and compare bit-exactly.");
+
+    m.def("encode_ppm", [](const bml::Grid& g) {
+        const auto bytes = bml::encode_ppm(g);
+        return py::bytes(reinterpret_cast<const char*>(bytes.data()), bytes.size());
+    }, py::arg("grid"));
+    m.def("write_ppm", [](const bml::Grid& g, const std::string& path) { bml::write_ppm(g, path); },
+          py::arg("grid"), py::arg("path"));
+
     m.def("vehicles_per_species", &bml::vehicles_per_species, py::arg("n"), py::arg("rho"));
 
     m.def("step", &step_many, py::arg("grid"), py::arg("steps") = 1,
@@ -217,6 +256,18 @@ PYBIND11_MODULE(_bml, m) {
                  const auto c = d.counts();
                  return py::make_tuple(c.lr, c.tb);
              })
+        .def("digest", &bml::DeviceLattice::digest, py::call_guard<py::gil_scoped_release>(),
+             "grid_digest of the device lattice, computed on the GPU")
+        .def("encode_ppm",
+             [](const bml::DeviceLattice& d) {
+                 std::vector<std::uint8_t> bytes;
+                 {
+                     py::gil_scoped_release nogil;
+                     bytes = d.encode_ppm();
+                 }
+                 return py::bytes(reinterpret_cast<const char*>(bytes.data()), bytes.size());
+             },
+             "encode_ppm of the device lattice (pixels expanded on the GPU)")
         .def("configure", &bml::DeviceLattice::configure, py::arg("block_steps") = 0,
              py::arg("strip_rows") = 0)
         .def("set_resident", &bml::DeviceLattice::set_resident, py::arg("mode"))
