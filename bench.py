@@ -132,8 +132,16 @@ def load_abi():
     lib.bml_dev_kernel_stats.argtypes = [vp, ctypes.POINTER(ctypes.c_int64),
                                          ctypes.POINTER(ctypes.c_double), ctypes.c_int]
     lib.bml_dev_info.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 5 + [ctypes.POINTER(ctypes.c_size_t)]
+    lib.bml_dev_last_launch.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 3
     lib.bml_dev_last_error.restype = ctypes.c_char_p
     return lib
+
+
+def last_launch(abi, h):
+    ns, items, grid = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    abi_check(abi, abi.bml_dev_last_launch(h, ctypes.byref(ns), ctypes.byref(items), ctypes.byref(grid)),
+              "last_launch")
+    return {"strips": ns.value, "items": items.value, "ctas": grid.value}
 
 
 def abi_check(lib, rc, what):
@@ -351,6 +359,7 @@ def run_b200(args, wl):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": kernel, "peak_source": peak_src,
+                     "launch_geometry": last_launch(abi, h) if kernel == "step_block_kernel" else None,
                      "resident_cluster": lat.resident_cluster,
                      "algorithmic_bytes_per_cell_update": BYTES_PER_CELL_UPDATE,
                      "launches": launches.value, "avg_launch_us": avg_launch_ms * 1e3,

@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <iterator>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -45,21 +46,18 @@
 namespace {
 
 constexpr int kHalo = 16;       // ghost rows per side == max steps fused per launch
-constexpr int kWarpsPerCta = 4;
+constexpr int kMaxWarpsPerCta = 12;  // step kernel: one CTA per SM, up to 3 warps per SMSP
 constexpr int kOutWords = 30;   // output words per warp in the haloed modes
 constexpr unsigned kFull = 0xffffffffu;
 
 #ifndef BML_FMA_SHIFTS
 #define BML_FMA_SHIFTS 0
 #endif
-#ifndef BML_STEP_MIN_CTAS
-#define BML_STEP_MIN_CTAS 3
+#ifndef BML_RES_RPW_FIRST
+#define BML_RES_RPW_FIRST 0  // preferred rows per warp of the resident kernel (0: by table)
 #endif
 #ifndef BML_IMAD_OR
 #define BML_IMAD_OR 1
-#endif
-#ifndef BML_RES_SKIP
-#define BML_RES_SKIP 0
 #endif
 
 enum Mode { kGeneric = 0, kAligned = 1, kFullRow = 2 };
@@ -111,7 +109,6 @@ struct StepArgs {
     int* error_flag;
     uint32_t two, half;  // 2 and 2^31, passed at run time so ptxas keeps IMAD (FMA pipe) shifts
     uint32_t one;        // 1, at run time: IMAD-issued ORs of disjoint planes (BML_IMAD_OR)
-    int sms;             // SM count (CTA wave of blockIdx, for the warp-slot rotation)
 };
 
 // --------------------------------------------------------------- device utils
@@ -350,19 +347,19 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
 }
 
 template <int K, int MODE, bool COUNT>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, BML_STEP_MIN_CTAS)
+__global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
 step_block_kernel(const StepArgs a) {
     const int lane = threadIdx.x & 31;
-    const int warps_total = gridDim.x * kWarpsPerCta;
-    __shared__ uint2 ring[kWarpsPerCta][kRing][32];
+    const int nwarps = blockDim.x >> 5;
+    const int warps_total = gridDim.x * nwarps;
+    __shared__ uint2 ring[kMaxWarpsPerCta][kRing][32];
     uint2 (*my_ring)[32] = ring[threadIdx.x >> 5];
 
-    // Warp-major item order: items 0..grid-1 go to one warp of every CTA, so
-    // when there are fewer items than warps they spread evenly over the SMs.
-    // The warp slot rotates with the CTA's wave (blockIdx / SMs), so the CTAs
-    // sharing an SM put their first busy warps on different SM sub-partitions.
-    const int slot = ((threadIdx.x >> 5) + blockIdx.x / a.sms) % kWarpsPerCta;
-    for (int item = slot * gridDim.x + blockIdx.x; item < a.items; item += warps_total) {
+    // One CTA per SM, 4u warps (u per SM sub-partition: warp w runs on SMSP
+    // w % 4). Warp-major item order: items 0..grid-1 go to warp 0 of every CTA,
+    // the next grid items to warp 1, ..., so a launch with fewer items than
+    // warps still spreads them evenly over the SMs and their sub-partitions.
+    for (int item = (threadIdx.x >> 5) * gridDim.x + blockIdx.x; item < a.items; item += warps_total) {
         const int strip = item / a.ncols;
         const int col = item - strip * a.ncols;
         StripCtx c;
@@ -509,6 +506,7 @@ step_block_kernel(const StepArgs a) {
 // refresh their ghost rows from the neighbours' shared memory (DSMEM) behind
 // one cluster barrier, so cross-SM synchronisation happens once per G steps.
 struct ResidentArgs {
+    uint32_t one;  // 1 at run time (IMAD-issued ORs of disjoint planes, BML_IMAD_OR)
     const uint2* src;
     uint2* dst;
     int n, W, pitch;
@@ -532,7 +530,6 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
     const int B = a.n / C;
     const int r0 = c * B;
     const int NW = blockDim.x >> 5;
-    const int E = NW * RPW;  // extended window rows = B + 2G
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int W = a.W;
     const bool lane_ok = lane < W;
@@ -581,23 +578,11 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
             }
         }
         for (int s = 0; s < kb; ++s) {
-            // ghost rows go stale one row per step from each window edge: a warp
-            // whose rows are all stale skips the arithmetic (warp-uniform)
-#if BML_RES_SKIP
-            const bool live = (w + 1) * RPW > s && w * RPW < E - s;
-#else
-            const bool live = true;
-            (void)E;
-#endif
             uint32_t Op[RPW];
             uint32_t lr_moved = 0;
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {  // LR phase, row-local
-                if (!live) {
-                    Op[i] = 0u;
-                    continue;
-                }
-                const uint32_t O = L[i] | T[i];
+                const uint32_t O = BML_IMAD_OR ? imad(L[i], a.one, T[i]) : (L[i] | T[i]);
                 const uint32_t Ll = __shfl_sync(kFull, L[i], left);
                 const uint32_t Or = __shfl_sync(kFull, O, right);
                 const uint32_t prevL = __funnelshift_l(Ll, L[i], 1);
@@ -609,7 +594,7 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
                     if (e >= G && e < G + B) lr_moved += __popc(vac & valid);
                 }
                 L[i] = inc | (L[i] & nextO);
-                Op[i] = L[i] | T[i];
+                Op[i] = BML_IMAD_OR ? imad(L[i], a.one, T[i]) : (L[i] | T[i]);
             }
             xT[par][w][lane] = T[RPW - 1];
             xO[par][w][lane] = Op[0];
@@ -619,7 +604,6 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
             uint32_t tb_moved = 0, lr_cnt = 0, tb_cnt = 0;
 #pragma unroll
             for (int i = RPW - 1; i >= 0; --i) {  // TB phase, top-down neighbours
-                if (!live) continue;
                 const uint32_t above = i > 0 ? T[i - 1] : t_up;
                 const uint32_t below = i < RPW - 1 ? Op[i + 1] : o_dn;
                 const uint32_t nt = (above & ~Op[i]) | (T[i] & below);
@@ -806,14 +790,14 @@ __global__ void __launch_bounds__(1024, 1) resident_p2p_kernel(const ResidentArg
         uint32_t lr_moved = 0;
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {  // LR phase
-            const uint32_t O = L[i] | T[i];
+            const uint32_t O = BML_IMAD_OR ? imad(L[i], a.one, T[i]) : (L[i] | T[i]);
             const uint32_t Ll = __shfl_sync(kFull, L[i], left);
             const uint32_t Or = __shfl_sync(kFull, O, right);
             const uint32_t prevL = __funnelshift_l(Ll, L[i], 1);
             const uint32_t nextO = __funnelshift_r(O, Or, 1);
             if (COUNT) lr_moved += __popc(L[i] & ~nextO & valid);
             L[i] = (prevL & ~O) | (L[i] & nextO);
-            Op[i] = L[i] | T[i];
+            Op[i] = BML_IMAD_OR ? imad(L[i], a.one, T[i]) : (L[i] | T[i]);
         }
         if (w == 0) st_async_u32(p ? up_mO1 : up_mO0, Op[0], p ? up_bar1 : up_bar0);
         if (w == NW - 1) st_async_u32(p ? dn_mT1 : dn_mT0, T[RPW - 1], p ? dn_bar1 : dn_bar0);
@@ -1119,6 +1103,8 @@ struct bml_dev {
     int resident = 1;        // 1: use the cluster-resident kernel when the lattice qualifies
     int resident_cluster = 0;  // cluster size actually used by the last resident launch
     int last_nstrips = 0, last_grid = 0, last_items = 0;  // last streaming launch
+    int ns_cache_k[kHalo + 1] = {};        // memoised choose_nstrips per block depth
+    int ns_cache_setting[kHalo + 1] = {};  // the strip_rows setting it was computed for
     int sms = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
@@ -1314,12 +1300,19 @@ int choose_nstrips(const bml_dev* d, int k, int warps_per_sm) {
 int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_stride) {
     StepKernel kern = pick(k, d->mode, count);
     if (!kern) return fail(BML_EINVAL, "unsupported block depth " + std::to_string(k));
-    int max_ctas_per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_ctas_per_sm, kern, kWarpsPerCta * 32, 0);
-    max_ctas_per_sm = std::max(1, max_ctas_per_sm);
+    // warps per SMSP the register file allows (3 at <= 168 registers/thread)
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    const int regs = std::max(1, (fa.numRegs + 7) / 8 * 8);
+    const int u_max = std::max(1, std::min(kMaxWarpsPerCta / 4, 65536 / (regs * 128)));
     // every strip has >= min(strip_rows, 16) rows, so for connected bands the
     // ghost-row sources of a band never straddle strips
-    const int nstrips = choose_nstrips(d, k, max_ctas_per_sm * kWarpsPerCta);
+    // the model scans every strip count: memoised per (k, strip setting)
+    if (d->ns_cache_k[k] <= 0 || d->ns_cache_setting[k] != d->strip_rows) {
+        d->ns_cache_k[k] = choose_nstrips(d, k, 4 * u_max);
+        d->ns_cache_setting[k] = d->strip_rows;
+    }
+    const int nstrips = d->ns_cache_k[k];
     const int strip = d->rows / nstrips;
     StepArgs a{};
     a.src = d->row0(d->cur);
@@ -1349,13 +1342,11 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
     a.two = 2u;
     a.half = 0x80000000u;
     a.one = 1u;
-    a.sms = d->sms;
 
-    // sms x m CTAs: every SM gets the same number of CTAs, the warp-major item
-    // order then spreads the items evenly over the SMs
-    const int m = std::min(max_ctas_per_sm,
-                           std::max(1, (a.items + d->sms * kWarpsPerCta - 1) / (d->sms * kWarpsPerCta)));
-    const int grid = std::max(1, std::min(d->sms * m, a.items));
+    // one CTA per SM with 4u warps, u = the warps per SMSP the items need
+    const int u = std::min(u_max, std::max(1, (a.items + 4 * d->sms - 1) / (4 * d->sms)));
+    const int grid = std::max(1, std::min(d->sms, a.items));
+    const int threads = 4 * u * 32;
     d->last_nstrips = nstrips;
     d->last_grid = grid;
     d->last_items = a.items;
@@ -1366,7 +1357,7 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
         e1 = take_event(d);
         cudaEventRecord(e0, d->stream);
     }
-    kern<<<grid, kWarpsPerCta * 32, 0, d->stream>>>(a);
+    kern<<<grid, threads, 0, d->stream>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "step_block_kernel launch");
     if (d->timing) {
@@ -1425,8 +1416,8 @@ bool resident_plan(const bml_dev* d, int cluster, int* ghost, int* rpw, int* war
     const int G = std::min(kResidentMaxGhost, std::max(1, d->block_steps));
     if (B < G) return false;
     const int E = B + 2 * G;
-    for (int r : {5, 4, 6, 3, 8, 2, 1}) {
-        if (E % r == 0 && E / r <= kResidentMaxWarps && E / r >= 1) {
+    for (int r : {BML_RES_RPW_FIRST, 5, 4, 6, 3, 8, 2, 1}) {
+        if (r > 0 && E % r == 0 && E / r <= kResidentMaxWarps && E / r >= 1) {
             *ghost = G;
             *rpw = r;
             *warps = E / r;
@@ -1470,6 +1461,7 @@ int launch_resident(bml_dev* d, long long steps, bool count, bool* used) {
             continue;
         }
         ResidentArgs ra{};
+        ra.one = 1u;
         ra.src = d->row0(d->cur);
         ra.dst = d->row0(d->cur ^ 1);
         ra.n = d->n;
@@ -1945,6 +1937,7 @@ int bml_dev_connect(bml_dev* d, const void* up_blob, const void* down_blob) {
     link_peer(d, ubp, static_cast<unsigned long long*>(uf), up.row_end - up.row_begin, true);
     link_peer(d, dbp, static_cast<unsigned long long*>(df), dn.row_end - dn.row_begin, false);
     d->connected = true;
+    std::fill(std::begin(d->ns_cache_k), std::end(d->ns_cache_k), 0);  // strip limits changed
     return BML_OK;
 }
 
@@ -1968,6 +1961,7 @@ int bml_dev_connect_local(bml_dev* d, bml_dev* up, bml_dev* down) {
     link_peer(d, up->buf, up->flags, up->rows, true);
     link_peer(d, down->buf, down->flags, down->rows, false);
     d->connected = true;
+    std::fill(std::begin(d->ns_cache_k), std::end(d->ns_cache_k), 0);  // strip limits changed
     return BML_OK;
 }
 

@@ -32,6 +32,9 @@ for n in args.n:
         lib.bml_dev_set_stream.argtypes = [vp, vp]
         lib.bml_dev_download.argtypes = [vp, vp, ctypes.c_size_t]
         lib.bml_dev_destroy.argtypes = [vp]
+        has_ll = hasattr(lib, "bml_dev_last_launch")
+        if has_ll:
+            lib.bml_dev_last_launch.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 3
         h = vp()
         assert lib.bml_dev_create(n, 0, ctypes.byref(h)) == 0
         stream = torch.cuda.Stream()
@@ -58,7 +61,12 @@ for n in args.n:
                 digest = int(out[: 1 << 20].sum()) + int(out.sum())
                 if ref is None:
                     ref = digest
+                geo = None
+                if has_ll:
+                    g3 = [ctypes.c_int() for _ in range(3)]
+                    lib.bml_dev_last_launch(h, *[ctypes.byref(x) for x in g3])
+                    geo = [x.value for x in g3]
                 print(json.dumps({"lib": path.split("/")[-1], "n": n, "block": k, "strip": r,
                                   "steps": steps * (1 + args.reps), "gcups": round(best, 1),
-                                  "checksum": digest}), flush=True)
+                                  "checksum": digest, "strips_items_ctas": geo}), flush=True)
         lib.bml_dev_destroy(h)
