@@ -53,6 +53,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef BML_FMA_SHIFTS
 #define BML_FMA_SHIFTS 0
 #endif
+#ifndef BML_STORE_V2
+#define BML_STORE_V2 1
+#endif
 #ifndef BML_RES_RPW_FIRST
 #define BML_RES_RPW_FIRST 0  // preferred rows per warp of the resident kernel (0: by table)
 #endif
@@ -109,6 +112,8 @@ struct StepArgs {
     int* error_flag;
     uint32_t two, half;  // 2 and 2^31, passed at run time so ptxas keeps IMAD (FMA pipe) shifts
     uint32_t one;        // 1, at run time: IMAD-issued ORs of disjoint planes (BML_IMAD_OR)
+    long long top_delta;  // words from row o's slot to its upper image (ghost row rows+o / up peer)
+    long long bot_delta;  // words from row o's slot to its lower image (ghost row o-rows / down peer)
 };
 
 // --------------------------------------------------------------- device utils
@@ -230,6 +235,7 @@ struct StripCtx {
     int lane, r_lo, r_hi, out_word;
     uint32_t valid;
     unsigned span;  // rows this lane stores (r_hi - r_lo, or 0 for ghost lanes)
+    uint2* outp;    // aligned modes, BML_STORE_V2: this lane's word of the row emitted next
 };
 
 // Final-stage output of row o: the row itself plus its ghost images (the
@@ -238,9 +244,21 @@ struct StripCtx {
 // most one image per side and every store is a predicated STG (no branches
 // around the shuffles of the next stage).
 template <int MODE>
-__device__ __forceinline__ void store_row(const StepArgs& a, const StripCtx& c, int o, uint32_t l,
+__device__ __forceinline__ void store_row(const StepArgs& a, StripCtx& c, int o, uint32_t l,
                                           uint32_t t) {
     const bool st = static_cast<unsigned>(o - c.r_lo) < c.span;
+#if BML_STORE_V2
+    if (MODE != kGeneric) {
+        // aligned modes: valid is 0 (ghost lane, span 0) or all ones, so no
+        // masking; one running row pointer, images at fixed deltas from it
+        const uint2 v = make_uint2(l, t);
+        if (st) *c.outp = v;
+        if (st && o < kHalo) c.outp[a.top_delta] = v;            // -> ghost row rows+o (or up peer)
+        if (st && o >= a.rows - kHalo) c.outp[a.bot_delta] = v;  // -> ghost row o-rows (or down peer)
+        c.outp += a.pitch;
+        return;
+    }
+#endif
     const uint2 v = make_uint2(l & c.valid, t & c.valid);
     if (MODE != kGeneric) {
         const long long off = static_cast<long long>(o) * a.pitch + c.out_word;
@@ -273,7 +291,7 @@ __device__ __forceinline__ void store_row(const StepArgs& a, const StripCtx& c, 
 
 template <int K, int MODE, bool COUNT, int P>
 __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const int j,
-                                          const StepArgs& a, const StripCtx& c) {
+                                          const StepArgs& a, StripCtx& c) {
     constexpr int P3 = P % 3, P2 = P % 2;
     q.xt[P3] = x.y;
 #pragma unroll
@@ -414,6 +432,7 @@ step_block_kernel(const StepArgs a) {
         // cp.async ring: row j lands in slot (j - j_begin) % kRing; kRing == the
         // unroll factor, so every slot index below is a compile-time constant
         const uint2* gsrc = a.src + static_cast<long long>(j_begin) * a.pitch + word;
+        c.outp = a.dst + static_cast<long long>(j_begin - 2 * K + 1) * a.pitch + c.out_word;
         int j_issue = j_begin;
         auto issue_to = [&](int slot_idx) {
             if (j_issue < j_load_end) cp_async8(&my_ring[slot_idx][lane], gsrc);
@@ -1260,19 +1279,19 @@ int check_errors(bml_dev* d) {
 
 // Strips per launch. A strip of R rows costs R + 3K - 1 pipeline iterations
 // of K stages (2K ghost rows + K-1 drain). Items (strips x warp columns) are
-// spread evenly over the SMs and their four sub-partitions (SMSPs; warp-major
-// order with slot rotation, see step_block_kernel). Per-SMSP time model, in
+// spread evenly over the SMs and their four sub-partitions (SMSPs; one CTA
+// per SM, warp-major order, see step_block_kernel). Per-SMSP time model, in
 // clocks for one pipeline iteration of each of its u warps at K = 16, measured
-// on B200 (profiles/r1_sweep_strips*.jsonl, ncu issue statistics): u = 1: 460
-// (one warp's K independent stage chains cannot fill the issue slots), u = 2:
-// 774, u = 3: 1050 (~350 per warp: the ALU pipe and issue slots saturate).
-// An SM runs ceil(items / SMs) warps' items in rounds of at most
-// warps_per_sm. Rows are split evenly over the strips.
+// on B200 (profiles/r1_sweep_strips*.jsonl): u = 1: 430 (one warp's K
+// independent stage chains cannot fill the issue slots), u = 2: 603, u = 3:
+// 826 (~275 per warp: ALU pipe and issue slots near saturation). An SM runs
+// ceil(items / SMs) warps' items in rounds of at most warps_per_sm. Rows are
+// split evenly over the strips.
 long long smsp_round_cost(long long w) {
     const long long u = (w + 3) / 4;
-    if (u <= 1) return 460;
-    if (u == 2) return 774;
-    return 1050 + (u - 3) * 350;
+    if (u <= 1) return 430;
+    if (u == 2) return 603;
+    return 826 + (u - 3) * 275;
 }
 
 int choose_nstrips(const bml_dev* d, int k, int warps_per_sm) {
@@ -1342,6 +1361,17 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
     a.two = 2u;
     a.half = 0x80000000u;
     a.one = 1u;
+    {
+        // image slots relative to a row's own slot (flat 64-bit address space,
+        // so the distance to a peer's buffer is a plain pointer difference)
+        const long long rp = static_cast<long long>(d->rows) * d->pitch;
+        const auto words_between = [](const uint2* from, const uint2* to) {
+            return static_cast<long long>(reinterpret_cast<intptr_t>(to) - reinterpret_cast<intptr_t>(from)) /
+                   static_cast<long long>(sizeof(uint2));
+        };
+        a.top_delta = d->connected ? words_between(a.dst, a.up_halo) : rp;
+        a.bot_delta = d->connected ? words_between(a.dst, a.down_halo) - rp : -rp;
+    }
 
     // one CTA per SM with 4u warps, u = the warps per SMSP the items need
     const int u = std::min(u_max, std::max(1, (a.items + 4 * d->sms - 1) / (4 * d->sms)));
