@@ -309,30 +309,26 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
 #else
         const uint32_t O = L | T;
 #endif
-#if BML_FMA_SHIFTS
-        // shifts on the FMA pipe (IMAD / IMAD.HI); the ALU pipe is the bottleneck
-        const uint32_t lc = __umulhi(L, a.two);   // L >> 31: carry into the right neighbour
-        const uint32_t oc = O * a.half;           // O << 31: carry into the left neighbour
-        uint32_t cl, cr;
-        if (MODE == kFullRow) {
-            cl = __shfl_sync(kFull, lc, (c.lane + 31) & 31);
-            cr = __shfl_sync(kFull, oc, (c.lane + 1) & 31);
-        } else {
-            cl = __shfl_up_sync(kFull, lc, 1);
-            cr = __shfl_down_sync(kFull, oc, 1);
-        }
-        const uint32_t prevL = L * a.two + cl;            // (L << 1) | carry
+        // BML_FMA_SHIFTS: 1 moves the prevL shift, 2 both shifts, to the FMA pipe
+        // (IMAD / IMAD.HI with run-time multipliers): fewer ALU-pipe ops, more issues
+#if BML_FMA_SHIFTS >= 1
+        const uint32_t lc = __umulhi(L, a.two);  // L >> 31: carry into the right neighbour
+        const uint32_t cl = MODE == kFullRow ? __shfl_sync(kFull, lc, (c.lane + 31) & 31)
+                                             : __shfl_up_sync(kFull, lc, 1);
+        const uint32_t prevL = L * a.two + cl;  // (L << 1) | carry
+#else
+        const uint32_t Ll = MODE == kFullRow ? __shfl_sync(kFull, L, (c.lane + 31) & 31)
+                                             : __shfl_up_sync(kFull, L, 1);
+        const uint32_t prevL = __funnelshift_l(Ll, L, 1);
+#endif
+#if BML_FMA_SHIFTS >= 2
+        const uint32_t oc = O * a.half;  // O << 31: carry into the left neighbour
+        const uint32_t cr = MODE == kFullRow ? __shfl_sync(kFull, oc, (c.lane + 1) & 31)
+                                             : __shfl_down_sync(kFull, oc, 1);
         const uint32_t nextO = __umulhi(O, a.half) | cr;  // (O >> 1) | carry (OR folds into LOP3)
 #else
-        uint32_t Ll, Or;
-        if (MODE == kFullRow) {
-            Ll = __shfl_sync(kFull, L, (c.lane + 31) & 31);
-            Or = __shfl_sync(kFull, O, (c.lane + 1) & 31);
-        } else {
-            Ll = __shfl_up_sync(kFull, L, 1);
-            Or = __shfl_down_sync(kFull, O, 1);
-        }
-        const uint32_t prevL = __funnelshift_l(Ll, L, 1);
+        const uint32_t Or = MODE == kFullRow ? __shfl_sync(kFull, O, (c.lane + 1) & 31)
+                                             : __shfl_down_sync(kFull, O, 1);
         const uint32_t nextO = __funnelshift_r(O, Or, 1);
 #endif
         const uint32_t Lp = (prevL & ~O) | (L & nextO);

@@ -7,6 +7,7 @@ GPU box (which has no /root/reference) can check the CUDA path against it.
     python tests/golden/make_goldens.py small      # seconds-to-a-minute configs
     python tests/golden/make_goldens.py big        # N=8192 (~5 min each, lanes)
     python tests/golden/make_goldens.py huge       # N=32768 / N=65536 (hours, lanes)
+    python tests/golden/make_goldens.py c3         # N=32768 only (~75 min, lanes)
 
 Every record holds the reference's init digest, final digest after `steps`
 full steps, the vehicle counts and (where metrics=1) the observer-path sums
@@ -63,6 +64,6 @@ def run(c, force=False):
 
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "small"
-    table = {"small": SMALL, "big": BIG, "huge": HUGE}[which]
+    table = {"small": SMALL, "big": BIG, "huge": HUGE, "c3": HUGE[:1]}[which]
     for c in table:
         run(c)
