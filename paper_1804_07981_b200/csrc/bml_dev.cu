@@ -50,9 +50,6 @@ constexpr int kMaxWarpsPerCta = 12;  // step kernel: one CTA per SM, up to 3 war
 constexpr int kOutWords = 30;   // output words per warp in the haloed modes
 constexpr unsigned kFull = 0xffffffffu;
 
-#ifndef BML_FMA_SHIFTS
-#define BML_FMA_SHIFTS 0
-#endif
 #ifndef BML_STORE_V2
 #define BML_STORE_V2 1
 #endif
@@ -110,7 +107,6 @@ struct StepArgs {
     int metrics_stride;
     int step_base;
     int* error_flag;
-    uint32_t two, half;  // 2 and 2^31, passed at run time so ptxas keeps IMAD (FMA pipe) shifts
     uint32_t one;        // 1, at run time: IMAD-issued ORs of disjoint planes (BML_IMAD_OR)
     long long top_delta;  // words from row o's slot to its upper image (ghost row rows+o / up peer)
     long long bot_delta;  // words from row o's slot to its lower image (ghost row o-rows / down peer)
@@ -251,10 +247,8 @@ __device__ __forceinline__ void store_row(const StepArgs& a, StripCtx& c, int o,
     if (MODE != kGeneric) {
         // aligned modes: valid is 0 (ghost lane, span 0) or all ones, so no
         // masking; one running row pointer, images at fixed deltas from it
-        const uint2 v = make_uint2(l, t);
-        if (st) *c.outp = v;
-        if (st && o < kHalo) c.outp[a.top_delta] = v;            // -> ghost row rows+o (or up peer)
-        if (st && o >= a.rows - kHalo) c.outp[a.bot_delta] = v;  // -> ghost row o-rows (or down peer)
+        // (ghost-row images are copied after the strip, copy_images)
+        if (st) *c.outp = make_uint2(l, t);  // (st.global.cg / inline st.global measured 2-4% slower)
         c.outp += a.pitch;
         return;
     }
@@ -289,6 +283,29 @@ __device__ __forceinline__ void store_row(const StepArgs& a, StripCtx& c, int o,
     }
 }
 
+// Aligned modes: after a strip, its rows among the band's first / last kHalo
+// rows are copied (re-read from L2, this thread's own stores) to their ghost
+// images: the band's own ghost rows (single band) or the neighbours' (peer
+// stores over NVLink), then the neighbour's flag is raised. Keeps the per-row
+// store in the pipeline a single predicated STG.
+__device__ __noinline__ void copy_images(const StepArgs& a, int r_lo, int r_hi, int out_word,
+                                         bool stores) {
+    const int top_end = min(r_hi, kHalo);
+    const int bot_begin = max(r_lo, a.rows - kHalo);
+    for (int o = r_lo; o < top_end; ++o) {
+        const long long off = static_cast<long long>(o) * a.pitch + out_word;
+        if (stores) a.dst[off + a.top_delta] = __ldcg(a.dst + off);  // -> ghost row rows+o (or up peer)
+    }
+    for (int o = bot_begin; o < r_hi; ++o) {
+        const long long off = static_cast<long long>(o) * a.pitch + out_word;
+        if (stores) a.dst[off + a.bot_delta] = __ldcg(a.dst + off);  // -> ghost row o-rows (or down peer)
+    }
+    if (!a.single_band) {
+        if (r_lo == 0) publish(a.up_flag);
+        if (r_hi == a.rows) publish(a.down_flag);
+    }
+}
+
 template <int K, int MODE, bool COUNT, int P>
 __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const int j,
                                           const StepArgs& a, StripCtx& c) {
@@ -309,28 +326,14 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
 #else
         const uint32_t O = L | T;
 #endif
-        // BML_FMA_SHIFTS: 1 moves the prevL shift, 2 both shifts, to the FMA pipe
-        // (IMAD / IMAD.HI with run-time multipliers): fewer ALU-pipe ops, more issues
-#if BML_FMA_SHIFTS >= 1
-        const uint32_t lc = __umulhi(L, a.two);  // L >> 31: carry into the right neighbour
-        const uint32_t cl = MODE == kFullRow ? __shfl_sync(kFull, lc, (c.lane + 31) & 31)
-                                             : __shfl_up_sync(kFull, lc, 1);
-        const uint32_t prevL = L * a.two + cl;  // (L << 1) | carry
-#else
+        // (funnel shifts stay on the ALU pipe: moving them to the FMA pipe as
+        // IMAD / IMAD.HI measured 13-24% slower, profiles/r1_sweep_fma_shifts_rejected.jsonl)
         const uint32_t Ll = MODE == kFullRow ? __shfl_sync(kFull, L, (c.lane + 31) & 31)
                                              : __shfl_up_sync(kFull, L, 1);
-        const uint32_t prevL = __funnelshift_l(Ll, L, 1);
-#endif
-#if BML_FMA_SHIFTS >= 2
-        const uint32_t oc = O * a.half;  // O << 31: carry into the left neighbour
-        const uint32_t cr = MODE == kFullRow ? __shfl_sync(kFull, oc, (c.lane + 1) & 31)
-                                             : __shfl_down_sync(kFull, oc, 1);
-        const uint32_t nextO = __umulhi(O, a.half) | cr;  // (O >> 1) | carry (OR folds into LOP3)
-#else
         const uint32_t Or = MODE == kFullRow ? __shfl_sync(kFull, O, (c.lane + 1) & 31)
                                              : __shfl_down_sync(kFull, O, 1);
+        const uint32_t prevL = __funnelshift_l(Ll, L, 1);
         const uint32_t nextO = __funnelshift_r(O, Or, 1);
-#endif
         const uint32_t Lp = (prevL & ~O) | (L & nextO);
 #if BML_IMAD_OR
         const uint32_t Op = imad(Lp, a.one, T);  // Lp, T disjoint after the LR phase
@@ -479,14 +482,16 @@ step_block_kernel(const StepArgs a) {
             pipe_iter<K, MODE, COUNT, 3>(q, next_row(P3{}, nx0, nx1), j + 3, a, c);
             pipe_iter<K, MODE, COUNT, 4>(q, next_row(P4{}, nx0, nx1), j + 4, a, c);
             pipe_iter<K, MODE, COUNT, 5>(q, next_row(P5{}, nx0, nx1), j + 5, a, c);
-            if (!a.single_band) {
-                // rows j-2K+1 .. j-2K+6 were just stored
+            if (MODE == kGeneric && !a.single_band) {
+                // rows j-2K+1 .. j-2K+6 were just stored (with their images)
                 const int o_last = j - 2 * K + 6;
                 if (c.r_lo == 0 && o_last >= kHalo - 1 && o_last - 6 < kHalo - 1) publish(a.up_flag);
                 if (c.r_hi == a.rows && o_last >= a.rows - 1 && o_last - 6 < a.rows - 1)
                     publish(a.down_flag);
             }
         }
+        if (MODE != kGeneric && (c.r_lo < kHalo || c.r_hi > a.rows - kHalo))
+            copy_images(a, c.r_lo, c.r_hi, c.out_word, c.span != 0u);
 
         if (MODE != kGeneric) cp_async_wait<0>();
         if (COUNT) {
@@ -1278,16 +1283,16 @@ int check_errors(bml_dev* d) {
 // spread evenly over the SMs and their four sub-partitions (SMSPs; one CTA
 // per SM, warp-major order, see step_block_kernel). Per-SMSP time model, in
 // clocks for one pipeline iteration of each of its u warps at K = 16, measured
-// on B200 (profiles/r1_sweep_strips*.jsonl): u = 1: 430 (one warp's K
-// independent stage chains cannot fill the issue slots), u = 2: 603, u = 3:
-// 826 (~275 per warp: ALU pipe and issue slots near saturation). An SM runs
+// on B200 (profiles/r1_sweep_edge.jsonl): u = 1: 355 (one warp's K
+// independent stage chains cannot fill the issue slots), u = 2: 585, u = 3:
+// 800 (~265 per warp: ALU pipe and issue slots near saturation). An SM runs
 // ceil(items / SMs) warps' items in rounds of at most warps_per_sm. Rows are
 // split evenly over the strips.
 long long smsp_round_cost(long long w) {
     const long long u = (w + 3) / 4;
-    if (u <= 1) return 430;
-    if (u == 2) return 603;
-    return 826 + (u - 3) * 275;
+    if (u <= 1) return 355;
+    if (u == 2) return 585;
+    return 800 + (u - 3) * 265;
 }
 
 int choose_nstrips(const bml_dev* d, int k, int warps_per_sm) {
@@ -1354,8 +1359,6 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
     a.metrics_stride = metrics_stride;
     a.step_base = step_base;
     a.error_flag = d->err + 1;
-    a.two = 2u;
-    a.half = 0x80000000u;
     a.one = 1u;
     {
         // image slots relative to a row's own slot (flat 64-bit address space,
