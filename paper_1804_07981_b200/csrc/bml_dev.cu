@@ -56,6 +56,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef BML_RES_RPW_FIRST
 #define BML_RES_RPW_FIRST 0  // preferred rows per warp of the resident kernel (0: by table)
 #endif
+#ifndef BML_RES_P2P_GHOST
+#define BML_RES_P2P_GHOST 1  // resident kernel: st.async ghost pushes + neighbour mbarriers
+#endif
 #ifndef BML_IMAD_OR
 #define BML_IMAD_OR 1
 #endif
@@ -513,6 +516,61 @@ step_block_kernel(const StepArgs a) {
     }
 }
 
+// ------------------------------------------------------------ cluster mbarrier helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint32_t bar, uint32_t tx_bytes) {
+    asm volatile(
+        "{ .reg .b64 st; mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1; }" ::"r"(bar),
+        "r"(tx_bytes)
+        : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Bounded wait: a lost handoff raises the error flag after ~2 s instead of
+// hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int* err) {
+    if (mbar_try(bar, parity)) return;
+    if (*reinterpret_cast<volatile int*>(err)) return;  // already failed: do not wait again
+    const long long t0 = clock64();
+    while (!mbar_try(bar, parity)) {
+        if (clock64() - t0 > 4000000000LL) {
+            atomicExch(err, 3);
+            return;
+        }
+    }
+}
+__device__ __forceinline__ void st_async_u64(uint32_t remote_addr, uint32_t lo, uint32_t hi,
+                                             uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.u32 [%0], {%1, %2}, [%3];" ::"r"(
+                     remote_addr),
+                 "r"(lo), "r"(hi), "r"(remote_bar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_u32(uint32_t remote_addr, uint32_t v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(remote_addr),
+                 "r"(v), "r"(remote_bar)
+                 : "memory");
+}
+
 // ------------------------------------------------------------ resident cluster kernel
 //
 // Small lattices (n % 32 == 0, W = n/32 <= 32) are latency-bound in the
@@ -560,6 +618,19 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
     __shared__ uint32_t xO[2][kResidentMaxWarps][32];  // first row's occupancy after LR
     __shared__ uint2 ghostb[2][2 * kResidentMaxGhost][32];  // [0,G): rows above, [G,2G): rows below
     __shared__ unsigned long long cnt[4][kResidentMaxGhost];
+#if BML_RES_P2P_GHOST
+    // ghost rows arrive by st.async from the two neighbours, completing bytes on
+    // gbar[block parity]: only those two CTAs synchronise, no cluster barrier
+    __shared__ __align__(8) unsigned long long gbar[2];
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&gbar[0]), 1);
+        mbar_init(smem_u32(&gbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    const uint32_t ghost_bytes = 2u * static_cast<uint32_t>(G) * 32u * sizeof(uint2);
+    const int up_rank = (c + C - 1) % C, dn_rank = (c + 1) % C;
+    cluster.sync();  // every CTA's barriers are initialised before the first remote store
+#endif
 
     uint32_t L[RPW], T[RPW];
 #pragma unroll
@@ -578,9 +649,18 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
 
     const uint32_t valid = lane_ok ? kFull : 0u;
     int par = 0, bp = 0;
+    long long blk = 0;
     for (long long done = 0; done < a.steps;) {
         const int kb = static_cast<int>(min(static_cast<long long>(G), a.steps - done));
+#if BML_RES_P2P_GHOST
+        if (threadIdx.x == 0) mbar_arm(smem_u32(&gbar[bp]), ghost_bytes);  // this block's pushes
         if (done > 0) {
+            // the previous block's ghost rows: only warps holding ghost rows wait
+            const bool holds_ghost = w * RPW < G || (w + 1) * RPW > G + B;
+            if (holds_ghost) mbar_wait(smem_u32(&gbar[bp ^ 1]), static_cast<uint32_t>(((blk - 1) >> 1) & 1), a.error_flag);
+#else
+        if (done > 0) {
+#endif
             // ghost rows pushed into this CTA's shared memory by the neighbours
             // before the last cluster barrier (local loads only)
 #pragma unroll
@@ -618,14 +698,8 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
             }
             xT[par][w][lane] = T[RPW - 1];
             xO[par][w][lane] = Op[0];
-            __syncthreads();
-            const uint32_t t_up = w > 0 ? xT[par][w - 1][lane] : 0u;
-            const uint32_t o_dn = w < NW - 1 ? xO[par][w + 1][lane] : kFull;
             uint32_t tb_moved = 0, lr_cnt = 0, tb_cnt = 0;
-#pragma unroll
-            for (int i = RPW - 1; i >= 0; --i) {  // TB phase, top-down neighbours
-                const uint32_t above = i > 0 ? T[i - 1] : t_up;
-                const uint32_t below = i < RPW - 1 ? Op[i + 1] : o_dn;
+            auto tb_row = [&](int i, uint32_t above, uint32_t below) {  // TB phase, one row
                 const uint32_t nt = (above & ~Op[i]) | (T[i] & below);
                 if (COUNT) {
                     const int e = w * RPW + i;
@@ -636,7 +710,13 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
                     }
                 }
                 T[i] = nt;
-            }
+            };
+            __syncthreads();
+            const uint32_t t_up = w > 0 ? xT[par][w - 1][lane] : 0u;
+            const uint32_t o_dn = w < NW - 1 ? xO[par][w + 1][lane] : kFull;
+#pragma unroll
+            for (int i = RPW - 1; i >= 0; --i)  // top-down neighbours
+                tb_row(i, i > 0 ? T[i - 1] : t_up, i < RPW - 1 ? Op[i + 1] : o_dn);
             if (COUNT) {
                 const unsigned v0 = __reduce_add_sync(kFull, lr_moved);
                 const unsigned v1 = __reduce_add_sync(kFull, tb_moved);
@@ -655,6 +735,22 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
         // stores, made visible by the release/acquire cluster barrier below):
         // first G owned rows -> the CTA above's rows-below slots, last G owned
         // rows -> the CTA below's rows-above slots
+#if BML_RES_P2P_GHOST
+        {
+            const uint32_t base = smem_u32(&ghostb[bp][0][0]);
+            const uint32_t up_base = mapa_u32(base, up_rank), dn_base = mapa_u32(base, dn_rank);
+            const uint32_t up_bar = mapa_u32(smem_u32(&gbar[bp]), up_rank);
+            const uint32_t dn_bar = mapa_u32(smem_u32(&gbar[bp]), dn_rank);
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int e = w * RPW + i;
+                if (e >= G && e < 2 * G)
+                    st_async_u64(up_base + static_cast<uint32_t>((e * 32 + lane) * 8), L[i], T[i], up_bar);
+                if (e >= B && e < B + G)
+                    st_async_u64(dn_base + static_cast<uint32_t>(((e - B) * 32 + lane) * 8), L[i], T[i], dn_bar);
+            }
+        }
+#else
         {
             uint2* up = cluster.map_shared_rank(&ghostb[bp][0][0], (c + C - 1) % C);
             uint2* dn = cluster.map_shared_rank(&ghostb[bp][0][0], (c + 1) % C);
@@ -666,6 +762,7 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
                 if (e >= B && e < B + G) dn[(e - B) * 32 + lane] = v;
             }
         }
+#endif
         if (COUNT) {
             __syncthreads();
             for (int t = threadIdx.x; t < 4 * kb; t += blockDim.x) {
@@ -675,10 +772,16 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
                 cnt[q][s] = 0ull;
             }
         }
+#if !BML_RES_P2P_GHOST
         cluster.sync();
+#endif
         bp ^= 1;
         done += kb;
+        ++blk;
     }
+#if BML_RES_P2P_GHOST
+    cluster.sync();  // no CTA leaves while a neighbour may still store into its shared memory
+#endif
     // owned rows back to global, plus the single-band ghost images
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
@@ -701,52 +804,6 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
 // receiver's mbarrier (256 B per step per CTA). Only the two boundary warps
 // ever wait, and only for their two neighbours: no cluster-wide barrier, no
 // redundant ghost-row arithmetic.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, int rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arm(uint32_t bar, uint32_t tx_bytes) {
-    asm volatile(
-        "{ .reg .b64 st; mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1; }" ::"r"(bar),
-        "r"(tx_bytes)
-        : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-// Bounded wait: a lost handoff raises the error flag after ~2 s instead of
-// hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int* err) {
-    if (mbar_try(bar, parity)) return;
-    if (*reinterpret_cast<volatile int*>(err)) return;  // already failed: do not wait again
-    const long long t0 = clock64();
-    while (!mbar_try(bar, parity)) {
-        if (clock64() - t0 > 4000000000LL) {
-            atomicExch(err, 3);
-            return;
-        }
-    }
-}
-__device__ __forceinline__ void st_async_u32(uint32_t remote_addr, uint32_t v, uint32_t remote_bar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(remote_addr),
-                 "r"(v), "r"(remote_bar)
-                 : "memory");
-}
 
 template <int RPW, bool COUNT>
 __global__ void __launch_bounds__(1024, 1) resident_p2p_kernel(const ResidentArgs a) {
