@@ -159,6 +159,22 @@ def ref_bench(n, rho, seed, steps, backend, threads, reps):
     return rec
 
 
+def alu_roofline(kernel, achieved_gcups, resident_cluster, sm_max_mhz, sms=148):
+    """The bound that actually limits the bit-plane kernels: the
+    ALU pipe. Per 32-cell stage the kernels issue 6 ALU-pipe instructions (4 LOP3
+    + 2 funnel shifts; the two ORs of disjoint planes go to the FMA pipe), and the
+    ALU pipe retires 2 warp-instructions per clock per SM: 2/6 x 1024 = 341
+    cell-updates per clock per SM. `achieved` is the dominant kernel's rate (its
+    event-timed launches), over the SMs it runs on (the resident kernel: one
+    cluster)."""
+    used = resident_cluster if kernel == "resident_kernel" and resident_cluster else sms
+    mhz = sm_max_mhz or 1965
+    peak = 2.0 / 6.0 * 1024 * used * mhz * 1e6 / 1e9
+    return {"bound": "alu", "achieved": achieved_gcups, "peak": peak, "unit": "Gcell-updates/s",
+            "frac": achieved_gcups / peak, "sms": used, "sm_mhz": mhz,
+            "alu_instructions_per_32_cell_stage": 6}
+
+
 def cpu_sample_plan(n, steps):
     """Bounded samples (~seconds each) of the same workload for the CPU arms."""
     cells = n * n
@@ -364,6 +380,8 @@ def run_b200(args, wl):
                      "algorithmic_bytes_per_cell_update": BYTES_PER_CELL_UPDATE,
                      "launches": launches.value, "avg_launch_us": avg_launch_ms * 1e3,
                      "kernel_share_of_step": kernel_share},
+        "roofline_alu": alu_roofline(kernel, cell_updates / (kms.value / 1e3) / 1e9,
+                                     lat.resident_cluster, clocks.summary().get("sm_max_mhz")),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": timed_launches,
@@ -416,15 +434,22 @@ def run_b200_multi(args, wl):
     import torch.distributed as dist
 
     import paper_1804_07981_b200 as bml
-    from paper_1804_07981_b200.dist import BandLattice, weak_scaled_n
+    from paper_1804_07981_b200.dist import BandLattice, combine_digest, weak_scaled_n
 
     n1, rho, seed, steps, desc = wl
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    local = local % ndev  # more ranks than GPUs only in tests: ranks share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    shared_gpu = world > ndev
+    if shared_gpu:  # NCCL refuses two ranks on one GPU; the data path does not use it anyway
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if shared_gpu else dev
     n = weak_scaled_n(n1, world)
     band = BandLattice(n, rank, world, local, block_steps=args.block, strip_rows=args.strip)
     # each rank draws its rows of the same reference-RNG lattice on its own GPU
@@ -438,7 +463,6 @@ def run_b200_multi(args, wl):
         for _ in range(args.warmup):
             band.step(steps)
     stream.synchronize()
-    band.enable_timing(True)
     band.kernel_stats(reset=True)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -455,9 +479,19 @@ def run_b200_multi(args, wl):
         torch.cuda.synchronize()
         dist.barrier()
         wall = time.perf_counter() - t0
+    timed_launches, _ = band.kernel_stats(reset=True)
+    # roofline pass, outside the timed region: per-launch CUDA events
+    band.enable_timing(True)
+    dist.barrier()
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            band.step(steps)
+    stream.synchronize()
     launches, kms = band.kernel_stats(reset=True)
+    band.enable_timing(False)
     my_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    t = torch.tensor([my_ms, kms / max(1, launches)], dtype=torch.float64, device=dev)
+    t = torch.tensor([my_ms, kms / max(1, launches)], dtype=torch.float64, device=red_dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, avg_launch_ms = float(t[0]), float(t[1])
     value = n * n * steps * args.steps / (total_ms / 1e3) / 1e9
@@ -475,8 +509,15 @@ def run_b200_multi(args, wl):
         band.step(steps)
         band.download_rows()
         e2e_times.append(time.perf_counter() - t1)
-    et = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+    et = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=red_dev)
     dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    # whole-torus digest and conservation after the last e2e run (device-side)
+    segs = [None] * world
+    dist.all_gather_object(segs, (rank, band.digest_segment(), band.counts()))
+    segs.sort()
+    digest = combine_digest([sg for _, sg, _ in segs])
+    k_total = sum(lr for _, _, (lr, _) in segs), sum(tb for _, _, (_, tb) in segs)
+    conserved = k_total == (bml.vehicles_per_species(n, rho),) * 2
     if rank == 0:
         line = {
             "metric": "Gcell-updates/sec", "value": value, "unit": "Gcell-updates/s",
@@ -487,7 +528,8 @@ def run_b200_multi(args, wl):
             "config": {"workload": desc + f" weak-scaled to n={n}", "n": n, "rho": rho, "seed": seed,
                        "steps_per_run": steps, "parallelism": f"row bands x{world}, NVLink peer ghost rows",
                        "l2": "flushed (256 MiB write) between bench steps",
-                       "block_steps": args.block, "layout": "bit-planes, 2 bits/cell"},
+                       "block_steps": args.block, "layout": "bit-planes, 2 bits/cell",
+                       "shared_gpu": shared_gpu},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "step_block_kernel",
                          "peak_source": peak_src, "launches_per_rank": launches,
@@ -495,7 +537,11 @@ def run_b200_multi(args, wl):
             "cpu_baseline": None,
             "e2e": {"value": n * n * steps * args.steps / float(et[0]) / 1e9, "unit": "Gcell-updates/s",
                     "h2d_bytes_per_step": n * n, "d2h_bytes_per_step": n * n},
-            "gpu_launches": launches * world, "wall_s": wall, "clocks": clocks.summary(),
+            "gpu_launches": timed_launches * world, "wall_s": wall, "clocks": clocks.summary(),
+            "final": {"digest": f"0x{digest:016x}", "vehicles": list(k_total), "conserved": conserved,
+                      "steps": steps,
+                      "note": "grid_digest of init_grid(n, rho, seed) after `steps` steps (the last e2e "
+                              "run), combined on rank 0 from the bands' device digest segments"},
         }
         print(json.dumps(line))
     band.close()

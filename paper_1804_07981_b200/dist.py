@@ -75,6 +75,9 @@ class _Abi:
         lib.bml_dev_connect.argtypes = [vp, vp, vp]
         lib.bml_dev_exchange_halos.argtypes = [vp]
         lib.bml_dev_init_random.argtypes = [vp, ctypes.c_double, ctypes.c_uint64]
+        lib.bml_dev_digest_segment.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
+        lib.bml_digest_finish.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_uint64)]
         lib.bml_dev_sync.argtypes = [vp]
         lib.bml_dev_set_stream.argtypes = [vp, vp]
         lib.bml_dev_configure.argtypes = [vp, ctypes.c_int, ctypes.c_int]
@@ -150,6 +153,12 @@ class BandLattice:
         self.abi.check(self.abi.lib.bml_dev_counts(self.h, ctypes.byref(a), ctypes.byref(b)), "counts")
         return a.value, b.value
 
+    def digest_segment(self):
+        """This band's grid_digest segment (6 words), computed on the device."""
+        seg = (ctypes.c_uint64 * 6)()
+        self.abi.check(self.abi.lib.bml_dev_digest_segment(self.h, seg), "digest_segment")
+        return list(seg)
+
     def set_stream(self, stream_ptr):
         self.abi.check(self.abi.lib.bml_dev_set_stream(self.h, ctypes.c_void_p(stream_ptr)), "set_stream")
 
@@ -176,6 +185,17 @@ class BandLattice:
             self.close()
         except Exception:
             pass
+
+
+def combine_digest(segments):
+    """grid_digest of the whole torus from every band's segment, in band (row) order."""
+    lib = _Abi().lib
+    flat = (ctypes.c_uint64 * (6 * len(segments)))(*[w for seg in segments for w in seg])
+    out = ctypes.c_uint64()
+    rc = lib.bml_digest_finish(flat, len(segments), ctypes.byref(out))
+    if rc != 0:
+        raise RuntimeError("bml_digest_finish failed")
+    return out.value
 
 
 def init_from_env():
