@@ -56,6 +56,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef BML_RES_RPW_FIRST
 #define BML_RES_RPW_FIRST 0  // preferred rows per warp of the resident kernel (0: by table)
 #endif
+#ifndef BML_PDL
+#define BML_PDL 1  // step kernel: programmatic dependent launch between consecutive blocks
+#endif
 #ifndef BML_RES_P2P_GHOST
 #define BML_RES_P2P_GHOST 1  // resident kernel: st.async ghost pushes + neighbour mbarriers
 #endif
@@ -369,6 +372,10 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
 template <int K, int MODE, bool COUNT>
 __global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
 step_block_kernel(const StepArgs a) {
+    if (BML_PDL) {
+        asm volatile("griddepcontrol.launch_dependents;");
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous launch's rows are final
+    }
     const int lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     const int warps_total = gridDim.x * nwarps;
@@ -1443,8 +1450,25 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
         e1 = take_event(d);
         cudaEventRecord(e0, d->stream);
     }
-    kern<<<grid, threads, 0, d->stream>>>(a);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e;
+    if (BML_PDL) {
+        // programmatic dependent launch: this grid may be scheduled while the
+        // previous one drains; the kernel waits (griddepcontrol.wait) before
+        // touching the lattice, so only the launch gap is hidden
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(static_cast<unsigned>(threads));
+        cfg.stream = d->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, a);
+    } else {
+        kern<<<grid, threads, 0, d->stream>>>(a);
+        e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return cuda_fail(e, "step_block_kernel launch");
     if (d->timing) {
         cudaEventRecord(e1, d->stream);
