@@ -50,17 +50,8 @@ constexpr int kMaxWarpsPerCta = 12;  // step kernel: one CTA per SM, up to 3 war
 constexpr int kOutWords = 30;   // output words per warp in the haloed modes
 constexpr unsigned kFull = 0xffffffffu;
 
-#ifndef BML_STORE_V2
-#define BML_STORE_V2 1
-#endif
-#ifndef BML_RES_RPW_FIRST
-#define BML_RES_RPW_FIRST 0  // preferred rows per warp of the resident kernel (0: by table)
-#endif
 #ifndef BML_PDL
 #define BML_PDL 1  // step kernel: programmatic dependent launch between consecutive blocks
-#endif
-#ifndef BML_RES_P2P_GHOST
-#define BML_RES_P2P_GHOST 1  // resident kernel: st.async ghost pushes + neighbour mbarriers
 #endif
 #ifndef BML_IMAD_OR
 #define BML_IMAD_OR 1
@@ -188,12 +179,7 @@ __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
 
 // Asynchronous 8-byte global->shared copies (LDGSTS) feeding a per-warp ring of
 // input rows, so each warp keeps kRing-1 rows of loads in flight.
-#ifndef BML_RING
-#define BML_RING 6
-#endif
-// BML_RING == 6 (the main loop's unroll factor) makes every slot index a
-// compile-time constant; 8 keeps one more row in flight with computed slots.
-constexpr int kRing = BML_RING;
+constexpr int kRing = 6;  // == the main loop's unroll factor: every slot index is a compile-time constant
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
@@ -237,7 +223,7 @@ struct StripCtx {
     int lane, r_lo, r_hi, out_word;
     uint32_t valid;
     unsigned span;  // rows this lane stores (r_hi - r_lo, or 0 for ghost lanes)
-    uint2* outp;    // aligned modes, BML_STORE_V2: this lane's word of the row emitted next
+    uint2* outp;    // aligned modes: this lane's word of the row emitted next
 };
 
 // Final-stage output of row o: the row itself plus its ghost images (the
@@ -249,7 +235,6 @@ template <int MODE>
 __device__ __forceinline__ void store_row(const StepArgs& a, StripCtx& c, int o, uint32_t l,
                                           uint32_t t) {
     const bool st = static_cast<unsigned>(o - c.r_lo) < c.span;
-#if BML_STORE_V2
     if (MODE != kGeneric) {
         // aligned modes: valid is 0 (ghost lane, span 0) or all ones, so no
         // masking; one running row pointer, images at fixed deltas from it
@@ -258,7 +243,6 @@ __device__ __forceinline__ void store_row(const StepArgs& a, StripCtx& c, int o,
         c.outp += a.pitch;
         return;
     }
-#endif
     const uint2 v = make_uint2(l & c.valid, t & c.valid);
     if (MODE != kGeneric) {
         const long long off = static_cast<long long>(o) * a.pitch + c.out_word;
@@ -457,14 +441,10 @@ step_block_kernel(const StepArgs a) {
                 nx0 = nx1;
                 nx1 = fetch(j_issue);
                 ++j_issue;
-            } else if (kRing == 6) {
+            } else {
                 cp_async_wait<kRing - 2>();
                 x = my_ring[P][lane];
                 issue_to((P + kRing - 1) % kRing);
-            } else {
-                cp_async_wait<kRing - 2>();
-                x = my_ring[(j_issue - (kRing - 1) - j_begin) & (kRing - 1)][lane];
-                issue_to((j_issue - j_begin) & (kRing - 1));
             }
             return x;
         };
@@ -587,9 +567,10 @@ __device__ __forceinline__ void st_async_u32(uint32_t remote_addr, uint32_t v, u
 // G ghost rows above and below (its "extended window", E = B + 2G rows,
 // RPW rows per warp, lane = word). Each step is computed on the whole
 // window in registers; adjacent warps exchange one boundary row per phase
-// through shared memory (one __syncthreads per step). Every G steps the CTAs
-// refresh their ghost rows from the neighbours' shared memory (DSMEM) behind
-// one cluster barrier, so cross-SM synchronisation happens once per G steps.
+// through shared memory (one __syncthreads per step). Every G steps each CTA
+// pushes its first and last G owned rows into the two neighbour CTAs' ghost
+// buffers with st.async (DSMEM), completing bytes on the receiver's mbarrier;
+// only the warps holding ghost rows wait, and only for their two neighbours.
 struct ResidentArgs {
     uint32_t one;  // 1 at run time (IMAD-issued ORs of disjoint planes, BML_IMAD_OR)
     const uint2* src;
@@ -625,7 +606,6 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
     __shared__ uint32_t xO[2][kResidentMaxWarps][32];  // first row's occupancy after LR
     __shared__ uint2 ghostb[2][2 * kResidentMaxGhost][32];  // [0,G): rows above, [G,2G): rows below
     __shared__ unsigned long long cnt[4][kResidentMaxGhost];
-#if BML_RES_P2P_GHOST
     // ghost rows arrive by st.async from the two neighbours, completing bytes on
     // gbar[block parity]: only those two CTAs synchronise, no cluster barrier
     __shared__ __align__(8) unsigned long long gbar[2];
@@ -637,7 +617,6 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
     const uint32_t ghost_bytes = 2u * static_cast<uint32_t>(G) * 32u * sizeof(uint2);
     const int up_rank = (c + C - 1) % C, dn_rank = (c + 1) % C;
     cluster.sync();  // every CTA's barriers are initialised before the first remote store
-#endif
 
     uint32_t L[RPW], T[RPW];
 #pragma unroll
@@ -659,15 +638,11 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
     long long blk = 0;
     for (long long done = 0; done < a.steps;) {
         const int kb = static_cast<int>(min(static_cast<long long>(G), a.steps - done));
-#if BML_RES_P2P_GHOST
         if (threadIdx.x == 0) mbar_arm(smem_u32(&gbar[bp]), ghost_bytes);  // this block's pushes
         if (done > 0) {
             // the previous block's ghost rows: only warps holding ghost rows wait
             const bool holds_ghost = w * RPW < G || (w + 1) * RPW > G + B;
             if (holds_ghost) mbar_wait(smem_u32(&gbar[bp ^ 1]), static_cast<uint32_t>(((blk - 1) >> 1) & 1), a.error_flag);
-#else
-        if (done > 0) {
-#endif
             // ghost rows pushed into this CTA's shared memory by the neighbours
             // before the last cluster barrier (local loads only)
 #pragma unroll
@@ -742,7 +717,6 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
         // stores, made visible by the release/acquire cluster barrier below):
         // first G owned rows -> the CTA above's rows-below slots, last G owned
         // rows -> the CTA below's rows-above slots
-#if BML_RES_P2P_GHOST
         {
             const uint32_t base = smem_u32(&ghostb[bp][0][0]);
             const uint32_t up_base = mapa_u32(base, up_rank), dn_base = mapa_u32(base, dn_rank);
@@ -757,19 +731,6 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
                     st_async_u64(dn_base + static_cast<uint32_t>(((e - B) * 32 + lane) * 8), L[i], T[i], dn_bar);
             }
         }
-#else
-        {
-            uint2* up = cluster.map_shared_rank(&ghostb[bp][0][0], (c + C - 1) % C);
-            uint2* dn = cluster.map_shared_rank(&ghostb[bp][0][0], (c + 1) % C);
-#pragma unroll
-            for (int i = 0; i < RPW; ++i) {
-                const int e = w * RPW + i;
-                const uint2 v = make_uint2(L[i], T[i]);
-                if (e >= G && e < 2 * G) up[e * 32 + lane] = v;
-                if (e >= B && e < B + G) dn[(e - B) * 32 + lane] = v;
-            }
-        }
-#endif
         if (COUNT) {
             __syncthreads();
             for (int t = threadIdx.x; t < 4 * kb; t += blockDim.x) {
@@ -779,16 +740,11 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
                 cnt[q][s] = 0ull;
             }
         }
-#if !BML_RES_P2P_GHOST
-        cluster.sync();
-#endif
         bp ^= 1;
         done += kb;
         ++blk;
     }
-#if BML_RES_P2P_GHOST
     cluster.sync();  // no CTA leaves while a neighbour may still store into its shared memory
-#endif
     // owned rows back to global, plus the single-band ghost images
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
@@ -1526,8 +1482,8 @@ bool resident_plan(const bml_dev* d, int cluster, int* ghost, int* rpw, int* war
     const int G = std::min(kResidentMaxGhost, std::max(1, d->block_steps));
     if (B < G) return false;
     const int E = B + 2 * G;
-    for (int r : {BML_RES_RPW_FIRST, 5, 4, 6, 3, 8, 2, 1}) {
-        if (r > 0 && E % r == 0 && E / r <= kResidentMaxWarps && E / r >= 1) {
+    for (int r : {5, 4, 6, 3, 8, 2, 1}) {
+        if (E % r == 0 && E / r <= kResidentMaxWarps && E / r >= 1) {
             *ghost = G;
             *rpw = r;
             *warps = E / r;
