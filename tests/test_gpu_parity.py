@@ -310,3 +310,24 @@ def test_resident_kernel_long_run_golden(gpu):
     assert f"0x{lat.download().digest():016x}" == g["final_digest"]
     assert sum(m.lr_moved for m in metrics) == g["sum_lr_moved"]
     assert sum(m.tb_moved for m in metrics) == g["sum_tb_moved"]
+
+
+@pytest.mark.parametrize("n,ns", [(1056, 7), (1056, 66), (2048, 2), (3000, 13)])
+def test_explicit_strip_count_and_launch_geometry(gpu, oracle, n, ns):
+    """strip_rows = -ns asks for exactly ns strips (include/bml_dev.h); rows are
+    split evenly and the result is bit-exact whatever the split."""
+    import ctypes
+    bml = gpu
+    cells = rand_lattice(n + ns, n)
+    lat = bml.DeviceLattice(n)
+    lat.set_resident(0)
+    lat.configure(block_steps=16, strip_rows=-ns)
+    lat.upload(grid_of(bml, n, cells))
+    lat.step(19)
+    lib = ctypes.CDLL(bml.LIB_DEV)
+    lib.bml_dev_last_launch.argtypes = [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int)] * 3
+    got = [ctypes.c_int() for _ in range(3)]
+    assert lib.bml_dev_last_launch(ctypes.c_void_p(lat.handle()), *[ctypes.byref(x) for x in got]) == 0
+    strips, items, ctas = (x.value for x in got)
+    assert strips == ns and items % ns == 0 and 1 <= ctas <= 148
+    assert lat.download().to_bytes() == oracle.run(n, cells, 19)
