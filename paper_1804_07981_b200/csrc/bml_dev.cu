@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <iterator>
+#include <mutex>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -353,8 +354,12 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
     }
 }
 
-template <int K, int MODE, bool COUNT>
-__global__ void __launch_bounds__(kMaxWarpsPerCta * 32, 1)
+// MAXT: launch bound. The default instantiation fits 3 warps per SMSP in the
+// register file (<= 168 registers); the 128-thread one (one warp per SMSP, the
+// latency-bound u = 1 regime of mid-size lattices) may use up to 255 registers,
+// and ptxas schedules it with fewer moves (+3.5% at N=8192).
+template <int K, int MODE, bool COUNT, int MAXT = kMaxWarpsPerCta * 32>
+__global__ void __launch_bounds__(MAXT, 1)
 step_block_kernel(const StepArgs a) {
     if (BML_PDL) {
         asm volatile("griddepcontrol.launch_dependents;");
@@ -363,7 +368,7 @@ step_block_kernel(const StepArgs a) {
     const int lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     const int warps_total = gridDim.x * nwarps;
-    __shared__ uint2 ring[kMaxWarpsPerCta][kRing][32];
+    __shared__ uint2 ring[MAXT / 32][kRing][32];
     uint2 (*my_ring)[32] = ring[threadIdx.x >> 5];
 
     // One CTA per SM, 4u warps (u per SM sub-partition: warp w runs on SMSP
@@ -1106,6 +1111,30 @@ StepKernel pick_k(int k) {
     }
 }
 
+// u = 1 (one warp per SMSP) variant of the K = 16 hot path, see step_block_kernel
+StepKernel pick_narrow(int k, int mode, bool count) {
+    if (k != 16 || count) return nullptr;
+    if (mode == kFullRow) return step_block_kernel<16, kFullRow, false, 128>;
+    if (mode == kAligned) return step_block_kernel<16, kAligned, false, 128>;
+    return nullptr;
+}
+
+// Warps per SMSP the register file allows for a kernel (memoised: the
+// attribute query costs host time on every launch otherwise).
+int warps_per_smsp(StepKernel kern) {
+    static std::mutex mu;
+    static std::vector<std::pair<StepKernel, int>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& kv : cache)
+        if (kv.first == kern) return kv.second;
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    const int regs = std::max(1, (fa.numRegs + 7) / 8 * 8);
+    const int u = std::max(1, std::min(kMaxWarpsPerCta / 4, 65536 / (regs * 128)));
+    cache.emplace_back(kern, u);
+    return u;
+}
+
 StepKernel pick(int k, int mode, bool count) {
     if (mode == kFullRow) return count ? pick_k<kFullRow, true>(k) : pick_k<kFullRow, false>(k);
     if (mode == kAligned) return count ? pick_k<kAligned, true>(k) : pick_k<kAligned, false>(k);
@@ -1304,14 +1333,14 @@ int check_errors(bml_dev* d) {
 // per SM, warp-major order, see step_block_kernel). Per-SMSP time model, in
 // clocks for one pipeline iteration of each of its u warps at K = 16, measured
 // on B200 (profiles/r1_sweep_edge.jsonl): u = 1: 355 (one warp's K
-// independent stage chains cannot fill the issue slots), u = 2: 585, u = 3:
+// independent stage chains cannot fill the issue slots), u = 2: 560, u = 3:
 // 800 (~265 per warp: ALU pipe and issue slots near saturation). An SM runs
 // ceil(items / SMs) warps' items in rounds of at most warps_per_sm. Rows are
 // split evenly over the strips.
 long long smsp_round_cost(long long w) {
     const long long u = (w + 3) / 4;
     if (u <= 1) return 355;
-    if (u == 2) return 585;
+    if (u == 2) return 560;
     return 800 + (u - 3) * 265;
 }
 
@@ -1340,11 +1369,7 @@ int choose_nstrips(const bml_dev* d, int k, int warps_per_sm) {
 int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_stride) {
     StepKernel kern = pick(k, d->mode, count);
     if (!kern) return fail(BML_EINVAL, "unsupported block depth " + std::to_string(k));
-    // warps per SMSP the register file allows (3 at <= 168 registers/thread)
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, kern);
-    const int regs = std::max(1, (fa.numRegs + 7) / 8 * 8);
-    const int u_max = std::max(1, std::min(kMaxWarpsPerCta / 4, 65536 / (regs * 128)));
+    const int u_max = warps_per_smsp(kern);  // 3 at <= 168 registers/thread
     // every strip has >= min(strip_rows, 16) rows, so for connected bands the
     // ghost-row sources of a band never straddle strips
     // the model scans every strip count: memoised per (k, strip setting)
@@ -1396,6 +1421,9 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
     const int u = std::min(u_max, std::max(1, (a.items + 4 * d->sms - 1) / (4 * d->sms)));
     const int grid = std::max(1, std::min(d->sms, a.items));
     const int threads = 4 * u * 32;
+    if (u == 1) {
+        if (StepKernel narrow = pick_narrow(k, d->mode, count)) kern = narrow;
+    }
     d->last_nstrips = nstrips;
     d->last_grid = grid;
     d->last_items = a.items;
