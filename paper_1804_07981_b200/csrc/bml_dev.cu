@@ -355,9 +355,9 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
 }
 
 // MAXT: launch bound. The default instantiation fits 3 warps per SMSP in the
-// register file (<= 168 registers); the 128-thread one (one warp per SMSP, the
-// latency-bound u = 1 regime of mid-size lattices) may use up to 255 registers,
-// and ptxas schedules it with fewer moves (+3.5% at N=8192).
+// register file (<= 168 registers); the 256-thread one (at most two warps per
+// SMSP, the latency-bound regime of mid-size lattices) may use up to 255
+// registers, and ptxas schedules it with fewer moves (+4% at N=8192).
 template <int K, int MODE, bool COUNT, int MAXT = kMaxWarpsPerCta * 32>
 __global__ void __launch_bounds__(MAXT, 1)
 step_block_kernel(const StepArgs a) {
@@ -1111,11 +1111,11 @@ StepKernel pick_k(int k) {
     }
 }
 
-// u = 1 (one warp per SMSP) variant of the K = 16 hot path, see step_block_kernel
+// u <= 2 (at most two warps per SMSP) variant of the K = 16 hot path, see step_block_kernel
 StepKernel pick_narrow(int k, int mode, bool count) {
     if (k != 16 || count) return nullptr;
-    if (mode == kFullRow) return step_block_kernel<16, kFullRow, false, 128>;
-    if (mode == kAligned) return step_block_kernel<16, kAligned, false, 128>;
+    if (mode == kFullRow) return step_block_kernel<16, kFullRow, false, 256>;
+    if (mode == kAligned) return step_block_kernel<16, kAligned, false, 256>;
     return nullptr;
 }
 
@@ -1421,7 +1421,7 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
     const int u = std::min(u_max, std::max(1, (a.items + 4 * d->sms - 1) / (4 * d->sms)));
     const int grid = std::max(1, std::min(d->sms, a.items));
     const int threads = 4 * u * 32;
-    if (u == 1) {
+    if (u <= 2) {
         if (StepKernel narrow = pick_narrow(k, d->mode, count)) kern = narrow;
     }
     d->last_nstrips = nstrips;
