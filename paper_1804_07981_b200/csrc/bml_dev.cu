@@ -1328,20 +1328,21 @@ int check_errors(bml_dev* d) {
 }
 
 // Strips per launch. A strip of R rows costs R + 3K - 1 pipeline iterations
-// of K stages (2K ghost rows + K-1 drain). Items (strips x warp columns) are
-// spread evenly over the SMs and their four sub-partitions (SMSPs; one CTA
-// per SM, warp-major order, see step_block_kernel). Per-SMSP time model, in
-// clocks for one pipeline iteration of each of its u warps at K = 16, measured
-// on B200 (profiles/r1_sweep_edge.jsonl): u = 1: 355 (one warp's K
-// independent stage chains cannot fill the issue slots), u = 2: 560, u = 3:
-// 800 (~265 per warp: ALU pipe and issue slots near saturation). An SM runs
-// ceil(items / SMs) warps' items in rounds of at most warps_per_sm. Rows are
-// split evenly over the strips.
+// of K stages (2K ghost rows + K-1 drain) plus about 16 iterations' worth of
+// per-item setup. Items (strips x warp columns) are spread evenly over the SMs
+// and their four sub-partitions (SMSPs; one CTA per SM, warp-major order, see
+// step_block_kernel). Per-SMSP time model, in clocks for one pipeline iteration
+// of each of its u warps at K = 16, measured on B200
+// (profiles/r1_sweep_narrow_u1.jsonl, r1_sweep_u2big.jsonl): u = 1: 330 (one
+// warp's K independent stage chains cannot fill the issue slots), u = 2: 515
+// (the 255-register instantiation), u = 3: 780 (~260 per warp: ALU pipe and
+// issue slots near saturation). An SM runs ceil(items / SMs) warps' items in
+// rounds of at most warps_per_sm. Rows are split evenly over the strips.
 long long smsp_round_cost(long long w) {
     const long long u = (w + 3) / 4;
-    if (u <= 1) return 355;
-    if (u == 2) return 560;
-    return 800 + (u - 3) * 265;
+    if (u <= 1) return 330;
+    if (u == 2) return 515;
+    return 780 + (u - 3) * 260;
 }
 
 int choose_nstrips(const bml_dev* d, int k, int warps_per_sm) {
@@ -1356,7 +1357,7 @@ int choose_nstrips(const bml_dev* d, int k, int warps_per_sm) {
         const long long r = (d->rows + ns - 1) / ns;
         const long long per_sm = (ns * cols + d->sms - 1) / d->sms;
         const long long full = per_sm / warps_per_sm, last = per_sm % warps_per_sm;
-        const long long cost = (r + 3 * k) * (full * smsp_round_cost(warps_per_sm) +
+        const long long cost = (r + 3 * k + 16) * (full * smsp_round_cost(warps_per_sm) +
                                               (last ? smsp_round_cost(last) : 0));
         if (best_cost < 0 || cost < best_cost) {
             best_cost = cost;
