@@ -100,8 +100,12 @@ int bml_dev_phase(bml_dev *dev, int phase, int64_t *moved);
  * arrays is nullable; when any is non-NULL, all requested arrays (length
  * `steps`) receive the per-step values of the reference observer loop
  * (engine.cpp:211-235): lr_moved, tb_moved, and the post-step lr/tb counts.
- * With counts requested, conservation is checked each step and a violation
- * returns BML_ECONSERVE. For bands, the values are this band's share. */
+ * The moved counts are popcounts fused into the step kernels. For a whole torus
+ * (single band) the rules conserve both species exactly, so the per-step counts
+ * are the counts measured before the run, and the final lattice is re-counted:
+ * any difference returns BML_ECONSERVE (engine.cpp:219-224's check). For row
+ * bands, whose counts change as TB vehicles cross band edges, the kernels count
+ * every step and the values are this band's share. */
 int bml_dev_step(bml_dev *dev, int64_t steps, int64_t *lr_moved, int64_t *tb_moved,
                  int64_t *lr_count, int64_t *tb_count);
 

@@ -82,7 +82,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 // ------------------------------------------------------------ dispatch table
 using StepKernel = void (*)(const StepArgs);
 
-template <int MODE, bool COUNT>
+template <int MODE, int COUNT>
 StepKernel pick_k(int k) {
     switch (k) {
         case 1: return step_block_kernel<1, MODE, COUNT>;
@@ -95,11 +95,13 @@ StepKernel pick_k(int k) {
 }
 
 // u <= 2 (at most two warps per SMSP) variant of the K = 16 hot path, see step_block_kernel
-StepKernel pick_narrow(int k, int mode, bool count) {
-    if (k != 16 || count) return nullptr;
-    if (mode == kFullRow) return step_block_kernel<16, kFullRow, false, 256>;
-    if (mode == kAligned) return step_block_kernel<16, kAligned, false, 256>;
-    return nullptr;
+StepKernel pick_narrow(int k, int mode, int count) {
+    if (k != 16 || count == 2) return nullptr;
+    if (mode == kFullRow) return count ? step_block_kernel<16, kFullRow, 1, 256>
+                                       : step_block_kernel<16, kFullRow, 0, 256>;
+    if (mode == kAligned) return count ? step_block_kernel<16, kAligned, 1, 256>
+                                       : step_block_kernel<16, kAligned, 0, 256>;
+    return count ? step_block_kernel<16, kGeneric, 1, 256> : step_block_kernel<16, kGeneric, 0, 256>;
 }
 
 // Warps per SMSP the register file allows for a kernel (memoised: the
@@ -118,10 +120,13 @@ int warps_per_smsp(StepKernel kern) {
     return u;
 }
 
-StepKernel pick(int k, int mode, bool count) {
-    if (mode == kFullRow) return count ? pick_k<kFullRow, true>(k) : pick_k<kFullRow, false>(k);
-    if (mode == kAligned) return count ? pick_k<kAligned, true>(k) : pick_k<kAligned, false>(k);
-    return count ? pick_k<kGeneric, true>(k) : pick_k<kGeneric, false>(k);
+// count: 0 no metrics, 1 moved counts, 2 moved counts + vehicle census
+StepKernel pick(int k, int mode, int count) {
+    if (mode == kFullRow)
+        return count == 2 ? pick_k<kFullRow, 2>(k) : count ? pick_k<kFullRow, 1>(k) : pick_k<kFullRow, 0>(k);
+    if (mode == kAligned)
+        return count == 2 ? pick_k<kAligned, 2>(k) : count ? pick_k<kAligned, 1>(k) : pick_k<kAligned, 0>(k);
+    return count == 2 ? pick_k<kGeneric, 2>(k) : count ? pick_k<kGeneric, 1>(k) : pick_k<kGeneric, 0>(k);
 }
 
 int largest_block_at_most(long long remaining, int cap) {
@@ -350,8 +355,9 @@ int choose_nstrips(const bml_dev* d, int k, int warps_per_sm) {
     return best;
 }
 
-int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_stride) {
-    StepKernel kern = pick(k, d->mode, count);
+int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int metrics_stride) {
+    const int metrics = count ? (census ? 2 : 1) : 0;
+    StepKernel kern = pick(k, d->mode, metrics);
     if (!kern) return fail(BML_EINVAL, "unsupported block depth " + std::to_string(k));
     const int u_max = warps_per_smsp(kern);  // 3 at <= 168 registers/thread
     // every strip has >= min(strip_rows, 16) rows, so for connected bands the
@@ -361,7 +367,10 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
         d->ns_cache_k[k] = choose_nstrips(d, k, 4 * u_max);
         d->ns_cache_setting[k] = d->strip_rows;
     }
-    const int nstrips = d->ns_cache_k[k];
+    int nstrips = d->ns_cache_k[k];
+    // metrics kernels pack two per-lane counters into 16-bit halves: a strip
+    // may hold at most 2047 rows (32 cells per lane and row)
+    if (count) nstrips = std::max(nstrips, (d->rows + 2046) / 2047);
     const int strip = d->rows / nstrips;
     StepArgs a{};
     a.src = d->row0(d->cur);
@@ -406,7 +415,7 @@ int launch_block(bml_dev* d, int k, bool count, int step_base, int metrics_strid
     const int grid = std::max(1, std::min(d->sms, a.items));
     const int threads = 4 * u * 32;
     if (u <= 2) {
-        if (StepKernel narrow = pick_narrow(k, d->mode, count)) kern = narrow;
+        if (StepKernel narrow = pick_narrow(k, d->mode, metrics)) kern = narrow;
     }
     d->last_nstrips = nstrips;
     d->last_grid = grid;
@@ -505,7 +514,9 @@ bool resident_plan(const bml_dev* d, int cluster, int* ghost, int* rpw, int* war
     return false;
 }
 
-int launch_resident(bml_dev* d, long long steps, bool count, bool* used) {
+// (single band only: its metrics never need the per-step census, see bml_dev_step)
+int launch_resident(bml_dev* d, long long steps, bool count, bool census, bool* used) {
+    (void)census;
     *used = false;
     for (int cluster : {16, 8, 4, 2, 1}) {
         int G = 0, rpw = 0, nw = 0;
@@ -881,9 +892,18 @@ int bml_dev_step(bml_dev* d, int64_t steps, int64_t* lr_moved, int64_t* tb_moved
     const bool count = lr_moved || tb_moved || lr_count || tb_count;
     if (count && steps > (1LL << 26))
         return fail(BML_EINVAL, "bml_dev_step: at most 2^26 steps per call with metrics");
+    // Vehicle counts (the reference's count_vehicles after every step). A whole
+    // torus conserves both species exactly (LR vehicles move within their row, TB
+    // vehicles within their column), so for a single band the per-step census is
+    // the count measured before the run, re-measured on the final lattice
+    // (BML_ECONSERVE on any difference): popcounting both planes after every step
+    // would triple the cost of the metrics path (the POPC pipe is the bottleneck).
+    // A row band's counts change as TB vehicles cross band edges, so bands count
+    // in the kernel.
+    const bool want_counts = lr_count || tb_count;
+    const bool census = want_counts && !d->single_band();
     int64_t lr0 = 0, tb0 = 0;
-    const bool check_conservation = (lr_count || tb_count) && d->single_band();
-    if (check_conservation) {
+    if (want_counts && !census) {
         if (int rc = bml_dev_counts(d, &lr0, &tb0)) return rc;
     }
     if (count) {
@@ -892,11 +912,11 @@ int bml_dev_step(bml_dev* d, int64_t steps, int64_t* lr_moved, int64_t* tb_moved
     }
     d->resident_cluster = 0;
     bool resident_used = false;
-    if (int rc = launch_resident(d, steps, count, &resident_used)) return rc;
+    if (int rc = launch_resident(d, steps, count, census, &resident_used)) return rc;
     long long done = resident_used ? steps : 0;
     while (done < steps) {
         const int k = largest_block_at_most(steps - done, d->block_steps);
-        if (int rc = launch_block(d, k, count, static_cast<int>(done), static_cast<int>(steps)))
+        if (int rc = launch_block(d, k, count, census, static_cast<int>(done), static_cast<int>(steps)))
             return rc;
         done += k;
     }
@@ -905,23 +925,20 @@ int bml_dev_step(bml_dev* d, int64_t steps, int64_t* lr_moved, int64_t* tb_moved
         BML_CUDA(cudaMemcpyAsync(h.data(), d->metrics, h.size() * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost, d->stream));
         BML_CUDA(cudaStreamSynchronize(d->stream));
+        if (want_counts && !census) {
+            int64_t lr1 = 0, tb1 = 0;
+            if (int rc = bml_dev_counts(d, &lr1, &tb1)) return rc;
+            if (lr1 != lr0 || tb1 != tb0)
+                return fail(BML_ECONSERVE, "conservation violated within steps 1.." +
+                                               std::to_string(steps) + ": lr " + std::to_string(lr1) +
+                                               "/" + std::to_string(lr0) + ", tb " +
+                                               std::to_string(tb1) + "/" + std::to_string(tb0));
+        }
         for (int64_t s = 0; s < steps; ++s) {
             if (lr_moved) lr_moved[s] = static_cast<int64_t>(h[s]);
             if (tb_moved) tb_moved[s] = static_cast<int64_t>(h[steps + s]);
-            if (lr_count) lr_count[s] = static_cast<int64_t>(h[2 * steps + s]);
-            if (tb_count) tb_count[s] = static_cast<int64_t>(h[3 * steps + s]);
-        }
-        if (check_conservation) {
-            for (int64_t s = 0; s < steps; ++s) {
-                if (static_cast<int64_t>(h[2 * steps + s]) != lr0 ||
-                    static_cast<int64_t>(h[3 * steps + s]) != tb0) {
-                    return fail(BML_ECONSERVE,
-                                "conservation violated at step " + std::to_string(s + 1) +
-                                    ": lr " + std::to_string(h[2 * steps + s]) + "/" +
-                                    std::to_string(lr0) + ", tb " +
-                                    std::to_string(h[3 * steps + s]) + "/" + std::to_string(tb0));
-                }
-            }
+            if (lr_count) lr_count[s] = census ? static_cast<int64_t>(h[2 * steps + s]) : lr0;
+            if (tb_count) tb_count[s] = census ? static_cast<int64_t>(h[3 * steps + s]) : tb0;
         }
         return check_errors(d);
     }

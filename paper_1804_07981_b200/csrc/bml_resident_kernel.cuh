@@ -190,8 +190,7 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
                     const int e = w * RPW + i;
                     if (e >= G && e < G + B) {
                         tb_moved += __popc(T[i] & ~below & valid);
-                        lr_cnt += __popc(L[i] & valid);
-                        tb_cnt += __popc(nt & valid);
+
                     }
                 }
                 T[i] = nt;
@@ -358,8 +357,7 @@ __global__ void __launch_bounds__(1024, 1) resident_p2p_kernel(const ResidentArg
             const uint32_t nt = (above & ~Op[i]) | (T[i] & below);
             if (COUNT) {
                 tb_moved += __popc(T[i] & ~below & valid);
-                lr_cnt += __popc(L[i] & valid);
-                tb_cnt += __popc(nt & valid);
+
             }
             T[i] = nt;
         }

@@ -114,7 +114,7 @@ __device__ __noinline__ void copy_images(const StepArgs& a, int r_lo, int r_hi, 
     }
 }
 
-template <int K, int MODE, bool COUNT, int P>
+template <int K, int MODE, int COUNT, int P>
 __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const int j,
                                           const StepArgs& a, StripCtx& c) {
     constexpr int P3 = P % 3, P2 = P % 2;
@@ -157,8 +157,9 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
             if (static_cast<unsigned>(rho - c.r_lo) < span) q.cm[s] += __popc(L & ~nextO & c.valid);
             if (static_cast<unsigned>(rho - 1 - c.r_lo) < span) {
                 q.cm[s] += static_cast<uint32_t>(__popc(tB & ~Op & c.valid)) << 16;
-                q.cc[s] += __popc(newL & c.valid) +
-                           (static_cast<uint32_t>(__popc(newT & c.valid)) << 16);
+                if (COUNT == 2)  // per-step vehicle census (row bands: TB vehicles cross bands)
+                    q.cc[s] += __popc(newL & c.valid) +
+                               (static_cast<uint32_t>(__popc(newT & c.valid)) << 16);
             }
         }
         q.oc[s] = Op;
@@ -175,7 +176,9 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
 // register file (<= 168 registers); the 256-thread one (at most two warps per
 // SMSP, the latency-bound regime of mid-size lattices) may use up to 255
 // registers, and ptxas schedules it with fewer moves (+4% at N=8192).
-template <int K, int MODE, bool COUNT, int MAXT = kMaxWarpsPerCta * 32>
+// COUNT: 0 no metrics; 1 moved counts per step; 2 also the per-step vehicle
+// census (row bands only, see bml_dev_step)
+template <int K, int MODE, int COUNT, int MAXT = kMaxWarpsPerCta * 32>
 __global__ void __launch_bounds__(MAXT, 1)
 step_block_kernel(const StepArgs a) {
     if (BML_PDL) {
@@ -311,8 +314,8 @@ step_block_kernel(const StepArgs a) {
             for (int s = 0; s < K; ++s) {
                 const unsigned v0 = __reduce_add_sync(kFull, q.cm[s] & 0xffffu);
                 const unsigned v1 = __reduce_add_sync(kFull, q.cm[s] >> 16);
-                const unsigned v2 = __reduce_add_sync(kFull, q.cc[s] & 0xffffu);
-                const unsigned v3 = __reduce_add_sync(kFull, q.cc[s] >> 16);
+                const unsigned v2 = COUNT == 2 ? __reduce_add_sync(kFull, q.cc[s] & 0xffffu) : 0u;
+                const unsigned v3 = COUNT == 2 ? __reduce_add_sync(kFull, q.cc[s] >> 16) : 0u;
                 if (lane == 0) {
                     unsigned long long* m = a.metrics + a.step_base + s;
                     if (v0) atomicAdd(m, static_cast<unsigned long long>(v0));
