@@ -8,7 +8,8 @@ GPU box (which has no /root/reference) can check the CUDA path against it.
     python tests/golden/make_goldens.py big        # N=8192 (~5 min each, lanes)
     python tests/golden/make_goldens.py huge       # N=32768 / N=65536 (hours, lanes)
     python tests/golden/make_goldens.py c3         # N=32768 only (~95 min, lanes)
-    python tests/golden/make_goldens.py c4short    # N=65536, 1000 steps (~50 min, 43 GB RAM)
+    python tests/golden/make_goldens.py c4short    # N=65536, 1000 steps (~45 min, 43 GB RAM)
+    python tests/golden/make_goldens.py c4         # N=65536, 10000 steps (~6 h, 43 GB RAM)
 
 Every record holds the reference's init digest, final digest after `steps`
 full steps, the vehicle counts and (where metrics=1) the observer-path sums
@@ -66,6 +67,7 @@ def run(c, force=False):
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "small"
     c4short = [dict(n=65536, rho=0.35, seed=1, steps=1000, metrics=0)]
-    table = {"small": SMALL, "big": BIG, "huge": HUGE, "c3": HUGE[:1], "c4short": c4short}[which]
+    table = {"small": SMALL, "big": BIG, "huge": HUGE, "c3": HUGE[:1], "c4short": c4short,
+             "c4": HUGE[1:]}[which]
     for c in table:
         run(c)
