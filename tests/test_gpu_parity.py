@@ -229,6 +229,24 @@ def test_row_bands_match_single_band(gpu, oracle, devices, n):
     assert [m.lr_moved for m in metrics] == lm
     assert [m.tb_moved for m in metrics] == tm
     assert [m.lr_count for m in metrics] == lc
+    assert [m.tb_count for m in metrics] == tc
+
+
+def test_metrics_with_tall_strips(gpu, oracle):
+    """The metrics kernels pack two per-lane counters into 16-bit halves; strips
+    taller than 2047 rows would overflow them, so the launch splits such strips
+    even when asked for one (bml_dev.cu launch_block)."""
+    bml = gpu
+    n, steps = 4160, 3
+    cells = oracle.init_grid(n, 0.45, 8)
+    lat = bml.DeviceLattice(n)
+    lat.configure(block_steps=16, strip_rows=n)  # one strip requested
+    lat.upload(grid_of(bml, n, cells))
+    metrics = lat.step_with_metrics(steps)
+    want, (lm, tm, lc, tc) = oracle.run(n, cells, steps, metrics=True)
+    assert lat.download().to_bytes() == want
+    assert [m.lr_moved for m in metrics] == lm and [m.tb_moved for m in metrics] == tm
+    assert [m.lr_count for m in metrics] == lc and [m.tb_count for m in metrics] == tc
 
 
 def test_row_bands_reject_thin_bands(gpu):
