@@ -170,6 +170,7 @@ struct bml_dev {
     uint8_t* staging = nullptr;          // rows * n bytes
     unsigned long long* scratch = nullptr;  // 4 words: counts / moved
     int* err = nullptr;                  // [0]: bad upload cell, [1]: flag timeout
+    int* err_host = nullptr;             // pinned copy of err (4 ints)
     unsigned long long* flags = nullptr;  // [0]: top (from up), [1]: bottom (from down)
     unsigned long long* metrics = nullptr;
     long long metrics_cap = 0;
@@ -291,6 +292,9 @@ int create_common(int n, int row_begin, int row_end, int device, bml_dev** out) 
         return bail(e, "cudaMalloc(scratch)");
     if ((e = cudaMalloc(&d->err, 4 * sizeof(int))) != cudaSuccess) return bail(e, "cudaMalloc(err)");
     if ((e = cudaMemset(d->err, 0, 4 * sizeof(int))) != cudaSuccess) return bail(e, "cudaMemset(err)");
+    if ((e = cudaMallocHost(&d->err_host, 4 * sizeof(int))) != cudaSuccess)
+        return bail(e, "cudaMallocHost(err_host)");
+    std::memset(d->err_host, 0, 4 * sizeof(int));
     if ((e = cudaMalloc(&d->flags, 2 * sizeof(unsigned long long))) != cudaSuccess)
         return bail(e, "cudaMalloc(flags)");
     if ((e = cudaMemset(d->flags, 0, 2 * sizeof(unsigned long long))) != cudaSuccess)
@@ -302,17 +306,27 @@ int create_common(int n, int row_begin, int row_end, int device, bml_dev** out) 
     return BML_OK;
 }
 
-int check_errors(bml_dev* d) {
-    int h[4] = {0, 0, 0, 0};
-    cudaError_t e = cudaMemcpyAsync(h, d->err, sizeof h, cudaMemcpyDeviceToHost, d->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "error-flag readback");
+// Device error flags -> pinned host words, enqueued on the handle's stream;
+// errors_after_sync() reads them once the caller has synchronised.
+cudaError_t enqueue_error_readback(bml_dev* d) {
+    return cudaMemcpyAsync(d->err_host, d->err, 4 * sizeof(int), cudaMemcpyDeviceToHost, d->stream);
+}
+
+int errors_after_sync(bml_dev* d) {
+    const int* h = d->err_host;
     if (h[1]) {
         cudaMemsetAsync(d->err, 0, 4 * sizeof(int), d->stream);
         return fail(BML_ECUDA, h[1] == 3 ? "resident kernel: DSMEM handoff timed out"
                                          : "halo flag wait timed out (neighbour band stalled)");
     }
     return BML_OK;
+}
+
+int check_errors(bml_dev* d) {
+    cudaError_t e = enqueue_error_readback(d);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "error-flag readback");
+    return errors_after_sync(d);
 }
 
 // Strips per launch. A strip of R rows costs R + 3K - 1 pipeline iterations
@@ -514,6 +528,38 @@ bool resident_plan(const bml_dev* d, int cluster, int* ghost, int* rpw, int* war
     return false;
 }
 
+// Whether `cluster` CTAs of `threads` threads of `kern` can be co-scheduled
+// (non-portable sizes > 8 enabled first). Memoised: the attribute and occupancy
+// queries cost more host time than a short resident run.
+bool cluster_launchable(ResidentKernel kern, int cluster, int threads) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<ResidentKernel, int>, bool>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& kv : cache)
+        if (kv.first.first == kern && kv.first.second == cluster) return kv.second;
+    bool ok = true;
+    if (cluster > 8 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        ok = false;
+    if (ok) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(cluster));
+        cfg.blockDim = dim3(static_cast<unsigned>(threads));
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int max_clusters = 0;
+        ok = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) == cudaSuccess && max_clusters >= 1;
+    }
+    if (!ok) (void)cudaGetLastError();
+    cache.emplace_back(std::make_pair(kern, cluster), ok);
+    return ok;
+}
+
 // (single band only: its metrics never need the per-step census, see bml_dev_step)
 int launch_resident(bml_dev* d, long long steps, bool count, bool census, bool* used) {
     (void)census;
@@ -524,14 +570,7 @@ int launch_resident(bml_dev* d, long long steps, bool count, bool census, bool* 
         ResidentKernel kern = d->resident == 2
                                   ? (count ? pick_p2p<true>(rpw) : pick_p2p<false>(rpw))
                                   : (count ? pick_resident<true>(rpw) : pick_resident<false>(rpw));
-        if (!kern) continue;
-        if (cluster > 8) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-                cudaSuccess) {
-                (void)cudaGetLastError();
-                continue;
-            }
-        }
+        if (!kern || !cluster_launchable(kern, cluster, 32 * nw)) continue;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(cluster));
         cfg.blockDim = dim3(static_cast<unsigned>(32 * nw));
@@ -544,11 +583,6 @@ int launch_resident(bml_dev* d, long long steps, bool count, bool census, bool* 
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        int max_clusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
-            (void)cudaGetLastError();
-            continue;
-        }
         ResidentArgs ra{};
         ra.one = 1u;
         ra.src = d->row0(d->cur);
@@ -630,6 +664,7 @@ int bml_dev_destroy(bml_dev* d) {
     cudaFree(d->staging);
     cudaFree(d->scratch);
     cudaFree(d->err);
+    if (d->err_host) cudaFreeHost(d->err_host);
     cudaFree(d->flags);
     cudaFree(d->metrics);
     for (auto& pr : d->pending) {
@@ -742,10 +777,9 @@ int bml_dev_upload(bml_dev* d, const uint8_t* src, size_t src_pitch) {
     if (d->single_band()) {
         if (int rc = fill_images(d, d->cur)) return rc;
     }
-    int bad = 0;
-    BML_CUDA(cudaMemcpyAsync(&bad, d->err, sizeof(int), cudaMemcpyDeviceToHost, d->stream));
+    BML_CUDA(enqueue_error_readback(d));
     BML_CUDA(cudaStreamSynchronize(d->stream));
-    if (bad) return fail(BML_EINVAL, "bml_dev_upload: cell value outside {0,1,2}");
+    if (d->err_host[0]) return fail(BML_EINVAL, "bml_dev_upload: cell value outside {0,1,2}");
     return BML_OK;
 }
 
@@ -760,8 +794,9 @@ int bml_dev_download(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
     BML_CUDA(cudaGetLastError());
     BML_CUDA(cudaMemcpy2DAsync(dst, dst_pitch, d->staging, d->n, d->n, d->rows,
                                cudaMemcpyDefault, d->stream));
+    BML_CUDA(enqueue_error_readback(d));  // one synchronisation for data and flags
     BML_CUDA(cudaStreamSynchronize(d->stream));
-    return check_errors(d);
+    return errors_after_sync(d);
 }
 
 int bml_dev_init_random_masked(bml_dev* d, double rho, uint64_t seed, uint64_t reject_mask) {
