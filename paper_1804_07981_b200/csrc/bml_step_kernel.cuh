@@ -16,9 +16,7 @@ namespace bml_k {
 // Software pipeline: stage s (step s+1 of the block) at loop index j consumes
 // row j-2s at time s (produced by stage s-1 one iteration earlier, so all K
 // stages of an iteration are independent) and emits row j-2s-1 at time s+1.
-// Stage K-1 therefore emits row j-2K+1 at time K. The loop is unrolled by two
-// and the TB window's two T registers swap roles by iteration parity, so the
-// loop-carried state never moves between registers.
+// Stage K-1 therefore emits row j-2K+1 at time K.
 // Pipeline state. Values live in modulo-indexed register slots so that the
 // loop (unrolled by 6 = lcm of the 3- and 2-iteration lifetimes) never moves a
 // value between registers:
@@ -44,50 +42,34 @@ struct StripCtx {
     uint2* outp;    // aligned modes: this lane's word of the row emitted next
 };
 
-// Final-stage output of row o: the row itself plus its ghost images (the
-// band's own ghost rows for a single band, or the neighbours' ghost rows for
-// connected bands). Aligned modes have n >= 32 > kHalo, so each row has at
-// most one image per side and every store is a predicated STG (no branches
-// around the shuffles of the next stage).
+// Final-stage output of row o (rows outside the strip, and ghost lanes, are
+// not stored).
+//  - Aligned modes: valid is 0 (ghost lane, span 0) or all ones, so no
+//    masking; one predicated store through a running row pointer. The ghost
+//    images of the band's first/last kHalo rows are written after the strip
+//    (copy_images). st.global.cg / inline st.global measured 2-4% slower.
+//  - Generic mode (n % 32 != 0): masked words, and each row's images (tiny n
+//    can have several per side) are stored here.
 template <int MODE>
 __device__ __forceinline__ void store_row(const StepArgs& a, StripCtx& c, int o, uint32_t l,
                                           uint32_t t) {
     const bool st = static_cast<unsigned>(o - c.r_lo) < c.span;
     if (MODE != kGeneric) {
-        // aligned modes: valid is 0 (ghost lane, span 0) or all ones, so no
-        // masking; one running row pointer, images at fixed deltas from it
-        // (ghost-row images are copied after the strip, copy_images)
-        if (st) *c.outp = make_uint2(l, t);  // (st.global.cg / inline st.global measured 2-4% slower)
+        if (st) *c.outp = make_uint2(l, t);
         c.outp += a.pitch;
         return;
     }
+    if (!st) return;
     const uint2 v = make_uint2(l & c.valid, t & c.valid);
-    if (MODE != kGeneric) {
-        const long long off = static_cast<long long>(o) * a.pitch + c.out_word;
-        if (st) a.dst[off] = v;
-        {
-            uint2* top_img = a.single_band ? a.dst + static_cast<long long>(a.rows) * a.pitch : a.up_halo;
-            uint2* bot_img = a.single_band ? a.dst - static_cast<long long>(a.rows) * a.pitch
-                                           : a.down_halo - static_cast<long long>(a.rows) * a.pitch;
-            if (st && o < kHalo) top_img[off] = v;            // row o -> ghost row rows+o (or up peer)
-            if (st && o >= a.rows - kHalo) bot_img[off] = v;  // row o -> ghost row o-rows (or down peer)
-        }
-        return;
-    }
     const long long off = static_cast<long long>(o) * a.pitch + c.out_word;
-    {
-        if (st) {
-            a.dst[off] = v;
-            if (a.single_band) {
-                for (int h = o - a.n; h >= -kHalo; h -= a.n)
-                    a.dst[static_cast<long long>(h) * a.pitch + c.out_word] = v;
-                for (int h = o + a.n; h < a.rows + kHalo; h += a.n)
-                    a.dst[static_cast<long long>(h) * a.pitch + c.out_word] = v;
-            } else {
-                if (o < kHalo) a.up_halo[off] = v;
-                if (o >= a.rows - kHalo) a.down_halo[off - static_cast<long long>(a.rows) * a.pitch] = v;
-            }
-        }
+    a.dst[off] = v;
+    if (a.single_band) {
+        for (int h = o - a.n; h >= -kHalo; h -= a.n) a.dst[static_cast<long long>(h) * a.pitch + c.out_word] = v;
+        for (int h = o + a.n; h < a.rows + kHalo; h += a.n)
+            a.dst[static_cast<long long>(h) * a.pitch + c.out_word] = v;
+    } else {
+        if (o < kHalo) a.up_halo[off] = v;
+        if (o >= a.rows - kHalo) a.down_halo[off - static_cast<long long>(a.rows) * a.pitch] = v;
     }
 }
 
