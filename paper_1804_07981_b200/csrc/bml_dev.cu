@@ -484,8 +484,20 @@ ResidentKernel pick_p2p(int rpw) {
     }
 }
 
+template <bool COUNT, int PACK>
+ResidentKernel pick_resident_packed(int rpw) {
+    switch (rpw) {
+        case 1: return resident_kernel<1, COUNT, PACK>;
+        case 2: return resident_kernel<2, COUNT, PACK>;
+        case 3: return resident_kernel<3, COUNT, PACK>;
+        case 4: return resident_kernel<4, COUNT, PACK>;
+        default: return nullptr;
+    }
+}
+
 template <bool COUNT>
-ResidentKernel pick_resident(int rpw) {
+ResidentKernel pick_resident(int rpw, int pack) {
+    if (pack == 2) return pick_resident_packed<COUNT, 2>(rpw);
     switch (rpw) {
         case 1: return resident_kernel<1, COUNT>;
         case 2: return resident_kernel<2, COUNT>;
@@ -499,10 +511,11 @@ ResidentKernel pick_resident(int rpw) {
 }
 
 // Geometry of the resident launch, or false if the lattice does not qualify.
-bool resident_plan(const bml_dev* d, int cluster, int* ghost, int* rpw, int* warps) {
+bool resident_plan(const bml_dev* d, int cluster, int* ghost, int* rpw, int* warps, int* pack) {
     if (!d->resident || !d->single_band() || d->connected) return false;
     if (d->n % 32 != 0 || d->W > 32 || d->n % cluster != 0) return false;
     const int B = d->n / cluster;
+    *pack = 1;
     if (d->resident == 2) {  // p2p variant: no ghost rows, B = warps * rpw
         for (int r : {4, 2, 8, 1}) {
             if (B % r == 0 && B / r <= kResidentMaxWarps) {
@@ -517,13 +530,27 @@ bool resident_plan(const bml_dev* d, int cluster, int* ghost, int* rpw, int* war
     const int G = std::min(kResidentMaxGhost, std::max(1, d->block_steps));
     if (B < G) return false;
     const int E = B + 2 * G;
-    for (int r : {5, 4, 6, 3, 8, 2, 1}) {
-        if (E % r == 0 && E / r <= kResidentMaxWarps && E / r >= 1) {
-            *ghost = G;
-            *rpw = r;
-            *warps = E / r;
-            return true;
+    // a half-warp-wide lattice (W = 16, n = 512) packs two rows into each
+    // register: +15% (profiles/r1_sweep_resident_pack.jsonl). Narrower ones
+    // (n <= 256) measured slower packed: with so few rows per CTA the warps'
+    // latency chains, not the lanes, are the limit.
+    static constexpr int kPackedOrder[] = {2, 1, 3, 4};
+    static constexpr int kWideOrder[] = {5, 4, 6, 3, 8, 2, 1};
+    const int packed = d->W == 16 ? 2 : 1;
+    for (int p : {packed, 1}) {
+        const int* order = p > 1 ? kPackedOrder : kWideOrder;
+        const int norder = p > 1 ? 4 : 7;
+        for (int oi = 0; oi < norder; ++oi) {
+            const int r = order[oi];
+            if (E % (r * p) == 0 && E / (r * p) <= kResidentMaxWarps) {
+                *ghost = G;
+                *rpw = r;
+                *warps = E / (r * p);
+                *pack = p;
+                return true;
+            }
         }
+        if (p == 1) break;
     }
     return false;
 }
@@ -565,11 +592,11 @@ int launch_resident(bml_dev* d, long long steps, bool count, bool census, bool* 
     (void)census;
     *used = false;
     for (int cluster : {16, 8, 4, 2, 1}) {
-        int G = 0, rpw = 0, nw = 0;
-        if (!resident_plan(d, cluster, &G, &rpw, &nw)) continue;
+        int G = 0, rpw = 0, nw = 0, pack = 1;
+        if (!resident_plan(d, cluster, &G, &rpw, &nw, &pack)) continue;
         ResidentKernel kern = d->resident == 2
                                   ? (count ? pick_p2p<true>(rpw) : pick_p2p<false>(rpw))
-                                  : (count ? pick_resident<true>(rpw) : pick_resident<false>(rpw));
+                                  : (count ? pick_resident<true>(rpw, pack) : pick_resident<false>(rpw, pack));
         if (!kern || !cluster_launchable(kern, cluster, 32 * nw)) continue;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(cluster));

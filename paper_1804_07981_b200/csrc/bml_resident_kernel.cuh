@@ -89,8 +89,15 @@ struct ResidentArgs {
 constexpr int kResidentMaxWarps = 32;
 constexpr int kResidentMaxGhost = 16;
 
-template <int RPW, bool COUNT>
+// PACK: rows per register. A lattice narrower than a warp (W = 32 / PACK words,
+// n = 256 -> PACK 4) packs PACK rows into the 32 lanes: lane = segment * W +
+// word, segment s of register i holding window row w * RPW * PACK + s * RPW + i.
+// Column wrap stays inside a segment; the row above / below an edge register
+// comes from the neighbouring segment by a W-lane shuffle, and only the first /
+// last segment talks to the neighbouring warps through shared memory.
+template <int RPW, bool COUNT, int PACK = 1>
 __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a) {
+    constexpr int SEG = 32 / PACK;  // lanes per row segment
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = static_cast<int>(cluster.num_blocks());
@@ -100,10 +107,13 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
     const int r0 = c * B;
     const int NW = blockDim.x >> 5;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int W = a.W;
-    const bool lane_ok = lane < W;
-    const int left = lane == 0 ? W - 1 : lane - 1;
-    const int right = lane + 1 >= W ? 0 : lane + 1;
+    const int W = a.W;  // == SEG when PACK > 1
+    const int seg = lane / SEG, word = lane % SEG;
+    const bool lane_ok = word < W;
+    const int left = seg * SEG + (word == 0 ? W - 1 : word - 1);
+    const int right = seg * SEG + (word + 1 >= W ? 0 : word + 1);
+    constexpr int RW = RPW * PACK;  // window rows per warp
+    auto erow = [&](int i) { return w * RW + seg * RPW + i; };  // this lane's window row of register i
 
     __shared__ uint32_t xT[2][kResidentMaxWarps][32];  // last row's T of each warp
     __shared__ uint32_t xO[2][kResidentMaxWarps][32];  // first row's occupancy after LR
@@ -117,17 +127,17 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
         mbar_init(smem_u32(&gbar[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    const uint32_t ghost_bytes = 2u * static_cast<uint32_t>(G) * 32u * sizeof(uint2);
+    const uint32_t ghost_bytes = 2u * static_cast<uint32_t>(G) * (PACK == 1 ? 32u : SEG) * sizeof(uint2);
     const int up_rank = (c + C - 1) % C, dn_rank = (c + 1) % C;
     cluster.sync();  // every CTA's barriers are initialised before the first remote store
 
     uint32_t L[RPW], T[RPW];
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
-        const int e = w * RPW + i;
+        const int e = erow(i);
         int row = (r0 - G + e) % a.n;
         if (row < 0) row += a.n;
-        const uint2 x = lane_ok ? a.src[static_cast<long long>(row) * a.pitch + lane] : make_uint2(0u, 0u);
+        const uint2 x = lane_ok ? a.src[static_cast<long long>(row) * a.pitch + word] : make_uint2(0u, 0u);
         L[i] = x.x;
         T[i] = x.y;
     }
@@ -144,19 +154,19 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
         if (threadIdx.x == 0) mbar_arm(smem_u32(&gbar[bp]), ghost_bytes);  // this block's pushes
         if (done > 0) {
             // the previous block's ghost rows: only warps holding ghost rows wait
-            const bool holds_ghost = w * RPW < G || (w + 1) * RPW > G + B;
+            const bool holds_ghost = w * RW < G || (w + 1) * RW > G + B;
             if (holds_ghost) mbar_wait(smem_u32(&gbar[bp ^ 1]), static_cast<uint32_t>(((blk - 1) >> 1) & 1), a.error_flag);
             // ghost rows pushed into this CTA's shared memory by the neighbours
             // before the last cluster barrier (local loads only)
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
-                const int e = w * RPW + i;
+                const int e = erow(i);
                 if (e < G) {
-                    const uint2 x = ghostb[bp ^ 1][e][lane];
+                    const uint2 x = ghostb[bp ^ 1][e][word];
                     L[i] = x.x;
                     T[i] = x.y;
                 } else if (e >= G + B) {
-                    const uint2 x = ghostb[bp ^ 1][G + (e - G - B)][lane];
+                    const uint2 x = ghostb[bp ^ 1][G + (e - G - B)][word];
                     L[i] = x.x;
                     T[i] = x.y;
                 }
@@ -175,19 +185,19 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
                 const uint32_t inc = prevL & ~O;
                 const uint32_t vac = L[i] & ~nextO;
                 if (COUNT) {
-                    const int e = w * RPW + i;
+                    const int e = erow(i);
                     if (e >= G && e < G + B) lr_moved += __popc(vac & valid);
                 }
                 L[i] = inc | (L[i] & nextO);
                 Op[i] = BML_IMAD_OR ? imad(L[i], a.one, T[i]) : (L[i] | T[i]);
             }
-            xT[par][w][lane] = T[RPW - 1];
-            xO[par][w][lane] = Op[0];
+            if (seg == PACK - 1) xT[par][w][word] = T[RPW - 1];  // the warp's last row
+            if (seg == 0) xO[par][w][word] = Op[0];              // the warp's first row
             uint32_t tb_moved = 0, lr_cnt = 0, tb_cnt = 0;
             auto tb_row = [&](int i, uint32_t above, uint32_t below) {  // TB phase, one row
                 const uint32_t nt = (above & ~Op[i]) | (T[i] & below);
                 if (COUNT) {
-                    const int e = w * RPW + i;
+                    const int e = erow(i);
                     if (e >= G && e < G + B) {
                         tb_moved += __popc(T[i] & ~below & valid);
 
@@ -195,9 +205,12 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
                 }
                 T[i] = nt;
             };
+            // rows across segment boundaries (PACK > 1): W-lane shuffles
+            const uint32_t t_seg = PACK > 1 ? __shfl_up_sync(kFull, T[RPW - 1], SEG) : 0u;
+            const uint32_t o_seg = PACK > 1 ? __shfl_down_sync(kFull, Op[0], SEG) : 0u;
             __syncthreads();
-            const uint32_t t_up = w > 0 ? xT[par][w - 1][lane] : 0u;
-            const uint32_t o_dn = w < NW - 1 ? xO[par][w + 1][lane] : kFull;
+            const uint32_t t_up = seg > 0 ? t_seg : (w > 0 ? xT[par][w - 1][word] : 0u);
+            const uint32_t o_dn = seg < PACK - 1 ? o_seg : (w < NW - 1 ? xO[par][w + 1][word] : kFull);
 #pragma unroll
             for (int i = RPW - 1; i >= 0; --i)  // top-down neighbours
                 tb_row(i, i > 0 ? T[i - 1] : t_up, i < RPW - 1 ? Op[i + 1] : o_dn);
@@ -226,11 +239,11 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
             const uint32_t dn_bar = mapa_u32(smem_u32(&gbar[bp]), dn_rank);
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
-                const int e = w * RPW + i;
+                const int e = erow(i);
                 if (e >= G && e < 2 * G)
-                    st_async_u64(up_base + static_cast<uint32_t>((e * 32 + lane) * 8), L[i], T[i], up_bar);
+                    st_async_u64(up_base + static_cast<uint32_t>((e * 32 + word) * 8), L[i], T[i], up_bar);
                 if (e >= B && e < B + G)
-                    st_async_u64(dn_base + static_cast<uint32_t>(((e - B) * 32 + lane) * 8), L[i], T[i], dn_bar);
+                    st_async_u64(dn_base + static_cast<uint32_t>(((e - B) * 32 + word) * 8), L[i], T[i], dn_bar);
             }
         }
         if (COUNT) {
@@ -250,13 +263,13 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
     // owned rows back to global, plus the single-band ghost images
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
-        const int e = w * RPW + i;
+        const int e = erow(i);
         if (e >= G && e < G + B && lane_ok) {
             const int row = r0 + e - G;
             const uint2 v = make_uint2(L[i], T[i]);
-            a.dst[static_cast<long long>(row) * a.pitch + lane] = v;
-            for (int h = row - a.n; h >= -kHalo; h -= a.n) a.dst[static_cast<long long>(h) * a.pitch + lane] = v;
-            for (int h = row + a.n; h < a.n + kHalo; h += a.n) a.dst[static_cast<long long>(h) * a.pitch + lane] = v;
+            a.dst[static_cast<long long>(row) * a.pitch + word] = v;
+            for (int h = row - a.n; h >= -kHalo; h -= a.n) a.dst[static_cast<long long>(h) * a.pitch + word] = v;
+            for (int h = row + a.n; h < a.n + kHalo; h += a.n) a.dst[static_cast<long long>(h) * a.pitch + word] = v;
         }
     }
 }
