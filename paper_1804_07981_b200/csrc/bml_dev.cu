@@ -527,7 +527,10 @@ bool resident_plan(const bml_dev* d, int cluster, int* ghost, int* rpw, int* war
         }
         return false;
     }
-    const int G = std::min(kResidentMaxGhost, std::max(1, d->block_steps));
+    // ghost depth = steps between neighbour exchanges: the block depth, capped at
+    // 8, the measured optimum (profiles/r1_sweep_1024_paths.jsonl: 4.04 vs 3.99
+    // Tcell/s at G = 16; fewer redundant ghost rows against more exchanges)
+    const int G = std::min(kResidentGhost, std::max(1, d->block_steps));
     if (B < G) return false;
     const int E = B + 2 * G;
     // a half-warp-wide lattice (W = 16, n = 512) packs two rows into each
