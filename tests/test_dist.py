@@ -66,7 +66,7 @@ def _gloo_worker(rank, world, port, out):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_blob_exchange_gloo(world):
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()  # no fork() of a CUDA-initialised process
     out = mgr.dict()
     mp.spawn(_gloo_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     for r in range(world):
@@ -106,7 +106,7 @@ def test_two_processes_one_gpu_ipc_bands(world, oracle):
     if bml.device_count() < 1:
         pytest.skip("no CUDA device")
     n, steps = 512, 45
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()  # no fork() of a CUDA-initialised process
     out = mgr.dict()
     mp.spawn(_gpu_worker, args=(world, _free_port(), n, steps, out), nprocs=world, join=True)
     got = b"".join(out[r] for r in range(world))
