@@ -1,0 +1,29 @@
+"""Row-band protocol overhead on ONE GPU: an n x n torus split into g bands (each a
+bml_dev band handle with in-kernel ghost-row exchange and flags, all on device 0)
+against the single-band run. The bands share the GPU's SMs, so the ideal is the
+single-band throughput; the gap is the cost of the band protocol (flag waits,
+image copies, smaller launches)."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1804_07981_b200 as bml  # noqa: E402
+
+for n, steps in ((8192, 2048), (32768, 320)):
+    ref = None
+    for g in (1, 2, 4, 8):
+        lat = bml.DeviceLattice(n, devices=g)
+        lat.init_random(0.35, 1)
+        lat.step(steps)
+        lat.synchronize()
+        t = time.perf_counter()
+        lat.step(steps)
+        lat.synchronize()
+        dt = time.perf_counter() - t
+        d = lat.digest()
+        ref = d if ref is None else ref
+        print(json.dumps({"n": n, "bands": g, "tcups": n * n * steps / dt / 1e12, "digest_equal": d == ref}),
+              flush=True)
+        del lat
