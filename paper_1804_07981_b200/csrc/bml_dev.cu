@@ -101,6 +101,7 @@ StepKernel pick_narrow(int k, int mode, int count) {
                                        : step_block_kernel<16, kFullRow, 0, 256>;
     if (mode == kAligned) return count ? step_block_kernel<16, kAligned, 1, 256>
                                        : step_block_kernel<16, kAligned, 0, 256>;
+    if (mode == kSeam) return count ? step_block_kernel<16, kSeam, 1, 256> : step_block_kernel<16, kSeam, 0, 256>;
     return count ? step_block_kernel<16, kGeneric, 1, 256> : step_block_kernel<16, kGeneric, 0, 256>;
 }
 
@@ -126,6 +127,8 @@ StepKernel pick(int k, int mode, int count) {
         return count == 2 ? pick_k<kFullRow, 2>(k) : count ? pick_k<kFullRow, 1>(k) : pick_k<kFullRow, 0>(k);
     if (mode == kAligned)
         return count == 2 ? pick_k<kAligned, 2>(k) : count ? pick_k<kAligned, 1>(k) : pick_k<kAligned, 0>(k);
+    if (mode == kSeam)
+        return count == 2 ? pick_k<kSeam, 2>(k) : count ? pick_k<kSeam, 1>(k) : pick_k<kSeam, 0>(k);
     return count == 2 ? pick_k<kGeneric, 2>(k) : count ? pick_k<kGeneric, 1>(k) : pick_k<kGeneric, 0>(k);
 }
 
@@ -191,7 +194,11 @@ struct bml_dev {
 
     uint2* row0(int parity) const { return buf[parity] + static_cast<long long>(kHalo) * pitch; }
     bool single_band() const { return rows == n && row_begin == 0; }
-    int ncols() const { return mode == kFullRow ? 1 : (W + kOutWords - 1) / kOutWords; }
+    int ncols() const {
+        if (mode == kFullRow) return 1;
+        const int out = mode == kSeam ? kSeamOutWords : kOutWords;
+        return (W + out - 1) / out;
+    }
 };
 
 namespace {
@@ -272,7 +279,7 @@ int create_common(int n, int row_begin, int row_end, int device, bml_dev** out) 
     d->device = device;
     const int nb = n - 32 * (d->W - 1);
     d->last_mask = nb == 32 ? kFull : ((1u << nb) - 1u);
-    d->mode = (n % 32 != 0) ? kGeneric : (d->W == 32 ? kFullRow : kAligned);
+    d->mode = (n % 32 != 0) ? (d->W >= 32 ? kSeam : kGeneric) : (d->W == 32 ? kFullRow : kAligned);
     cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, device);
 
     auto bail = [&](cudaError_t err, const char* what) {

@@ -10,10 +10,10 @@
 
 namespace bml_k {
 
-
 constexpr int kHalo = 16;       // ghost rows per side == max steps fused per launch
 constexpr int kMaxWarpsPerCta = 12;  // step kernel: one CTA per SM, up to 3 warps per SMSP
-constexpr int kOutWords = 30;   // output words per warp in the haloed modes
+constexpr int kOutWords = 30;      // output words per warp in the haloed modes
+constexpr int kSeamOutWords = 28;  // kSeam: output words per warp (two ghost words per side)
 constexpr unsigned kFull = 0xffffffffu;
 
 #ifndef BML_PDL
@@ -23,7 +23,12 @@ constexpr unsigned kFull = 0xffffffffu;
 #define BML_IMAD_OR 1
 #endif
 
-enum Mode { kGeneric = 0, kAligned = 1, kFullRow = 2 };
+// kGeneric: n % 32 != 0 with rows narrower than a warp's span (n < 993): cells
+//   gathered across the seam, register prefetch. kSeam: n % 32 != 0, W >= 32:
+//   aligned row words through the cp.async ring, seam windows rebuilt with two
+//   shuffles and a funnel shift (28 output words per warp, 2 ghost words per
+//   side). kAligned: n % 32 == 0. kFullRow: W == 32 (one warp per row).
+enum Mode { kGeneric = 0, kAligned = 1, kFullRow = 2, kSeam = 3 };
 
 // ---------------------------------------------------------------- kernel args
 struct StepArgs {

@@ -38,6 +38,10 @@ struct PipeState {
 struct StripCtx {
     int lane, r_lo, r_hi, out_word;
     uint32_t valid;
+    // kSeam: this lane's window = funnel_r(lo, hi, sh) with lo = own word <<
+    // pre (or the left lane's word), hi = the right lane's word (or own word)
+    int seam_pre, seam_sh;
+    bool seam_left;
     unsigned span;  // rows this lane stores (r_hi - r_lo, or 0 for ghost lanes)
     uint2* outp;    // aligned modes: this lane's word of the row emitted next
 };
@@ -55,7 +59,11 @@ __device__ __forceinline__ void store_row(const StepArgs& a, StripCtx& c, int o,
                                           uint32_t t) {
     const bool st = static_cast<unsigned>(o - c.r_lo) < c.span;
     if (MODE != kGeneric) {
-        if (st) *c.outp = make_uint2(l, t);
+        if (MODE == kSeam) {  // the last word is partial: keep its padding bits zero
+            if (st) *c.outp = make_uint2(l & c.valid, t & c.valid);
+        } else {
+            if (st) *c.outp = make_uint2(l, t);
+        }
         c.outp += a.pitch;
         return;
     }
@@ -71,6 +79,16 @@ __device__ __forceinline__ void store_row(const StepArgs& a, StripCtx& c, int o,
         if (o < kHalo) a.up_halo[off] = v;
         if (o >= a.rows - kHalo) a.down_halo[off - static_cast<long long>(a.rows) * a.pitch] = v;
     }
+}
+
+// kSeam: rebuild this lane's 32-cell window across the torus seam from its own
+// aligned row word and its neighbours' (see StripCtx).
+__device__ __forceinline__ uint32_t seam_window(uint32_t v, const StripCtx& c) {
+    const uint32_t right = __shfl_down_sync(kFull, v, 1);
+    const uint32_t left = __shfl_up_sync(kFull, v, 1);
+    const uint32_t lo = c.seam_left ? left : (v << c.seam_pre);
+    const uint32_t hi = c.seam_left ? v : right;
+    return __funnelshift_r(lo, hi, c.seam_sh);
 }
 
 // Aligned modes: after a strip, its rows among the band's first / last kHalo
@@ -189,15 +207,35 @@ step_block_kernel(const StepArgs a) {
         int word = lane, c0 = 0;
         c.out_word = lane;
         c.valid = kFull;
+        c.seam_pre = c.seam_sh = 0;
+        c.seam_left = false;
         if (MODE != kFullRow) {
-            const int w = col * kOutWords + lane - 1;
-            const bool is_out = lane >= 1 && lane <= kOutWords && w < a.W;
+            constexpr int kOut = MODE == kSeam ? kSeamOutWords : kOutWords;
+            constexpr int kLead = MODE == kSeam ? 2 : 1;  // ghost words on each side
+            const int w = col * kOut + lane - kLead;
+            const bool is_out = lane >= kLead && lane < kLead + kOut && w < a.W;
             c.out_word = w;
             c.valid = is_out ? (w == a.W - 1 ? a.last_mask : kFull) : 0u;
             word = ((w % a.W) + a.W) % a.W;
-            long long cc = (32LL * w) % a.n;
-            if (cc < 0) cc += a.n;
-            c0 = static_cast<int>(cc);
+            if (MODE == kGeneric) {
+                long long cc = (32LL * w) % a.n;
+                if (cc < 0) cc += a.n;
+                c0 = static_cast<int>(cc);
+            }
+            if (MODE == kSeam) {
+                // window of cells [32w, 32w + 32) mod n from the aligned row words;
+                // nb = cells in the last (partial) word. W >= 32, so a warp wraps once.
+                const int nb = a.n - 32 * (a.W - 1);
+                if (w == a.W - 1) {  // last word, then the row's first cells
+                    c.seam_pre = 32 - nb;
+                    c.seam_sh = 32 - nb;
+                } else if (w >= a.W) {  // past the end: word w-W shifted by 32-nb
+                    c.seam_sh = 32 - nb;
+                } else if (w == -1) {  // before the start: the row's last 32 cells
+                    c.seam_left = true;
+                    c.seam_sh = nb;
+                }
+            }
         }
 
         c.span = c.valid ? static_cast<unsigned>(c.r_hi - c.r_lo) : 0u;
@@ -252,6 +290,7 @@ step_block_kernel(const StepArgs a) {
                 cp_async_wait<kRing - 2>();
                 x = my_ring[P][lane];
                 issue_to((P + kRing - 1) % kRing);
+                if (MODE == kSeam) x = make_uint2(seam_window(x.x, c), seam_window(x.y, c));
             }
             return x;
         };

@@ -349,3 +349,28 @@ def test_explicit_strip_count_and_launch_geometry(gpu, oracle, n, ns):
     strips, items, ctas = (x.value for x in got)
     assert strips == ns and items % ns == 0 and 1 <= ctas <= 148
     assert lat.download().to_bytes() == oracle.run(n, cells, 19)
+
+
+@pytest.mark.parametrize("n", [993, 1000, 1023, 1025, 1100, 2047, 3000, 4099])
+@pytest.mark.parametrize("block", [1, 4, 16])
+def test_seam_mode_sizes(gpu, oracle, n, block):
+    """n % 32 != 0 with W >= 32 runs the kSeam mode: aligned words through the
+    cp.async ring, seam windows rebuilt by shuffles (bml_kernels_common.cuh)."""
+    bml = gpu
+    cells = rand_lattice(n * 7 + block, n)
+    lat = bml.DeviceLattice(n)
+    lat.configure(block_steps=block)
+    lat.upload(grid_of(bml, n, cells))
+    lat.step(37)
+    assert lat.download().to_bytes() == oracle.run(n, cells, 37)
+
+
+@pytest.mark.parametrize("n,bands", [(1100, 2), (3000, 3)])
+def test_seam_mode_bands_and_metrics(gpu, oracle, n, bands):
+    bml = gpu
+    cells = oracle.init_grid(n, 0.4, n)
+    final, metrics = bml.simulate(grid_of(bml, n, cells), 19, devices=bands)
+    want, (lm, tm, lc, tc) = oracle.run(n, cells, 19, metrics=True)
+    assert final.to_bytes() == want
+    assert [m.lr_moved for m in metrics] == lm and [m.tb_moved for m in metrics] == tm
+    assert [m.lr_count for m in metrics] == lc and [m.tb_count for m in metrics] == tc
