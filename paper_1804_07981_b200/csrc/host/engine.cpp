@@ -31,12 +31,6 @@ inline void ok(int rc, const char* what) {
     if (rc != BML_OK) raise(rc, what);
 }
 
-[[noreturn]] void not_provided(std::string_view where, Backend b) {
-    throw std::invalid_argument(std::string(where) + ": backend '" + std::string(backend_name(b)) +
-                                "' is a reference CPU engine and is not part of this build; "
-                                "use backend 'b200'");
-}
-
 }  // namespace
 
 std::string_view backend_name(Backend b) {
@@ -316,7 +310,17 @@ void check_pair(std::string_view where, const GridPair& pair, Backend backend, i
         throw std::invalid_argument(std::string(where) + ": backend '" +
                                     std::string(backend_name(backend)) +
                                     "' does not support threads > 1");
-    if (backend != Backend::B200) not_provided(where, backend);
+    // The reference backend names keep the reference's layout contract
+    // (engine.cpp:157-162: naive wants a dense grid, the others a halo grid);
+    // the phase itself runs on the device engine, as for b200, which takes
+    // either layout.
+    if (backend != Backend::B200) {
+        const bool want_halo = backend != Backend::ScalarNaive;
+        if (pair.cur.has_halo() != want_halo)
+            throw std::invalid_argument(std::string(where) + ": backend '" +
+                                        std::string(backend_name(backend)) +
+                                        (want_halo ? "' requires a halo grid" : "' requires a dense grid"));
+    }
 }
 
 }  // namespace
@@ -342,7 +346,7 @@ void step(Backend backend, GridPair& pair, int threads) {
 Grid run(const SimConfig& cfg, GridPair& pair, const StepObserver& observer) {
     validate(cfg);
     if (pair.cur.n() != cfg.n) throw std::invalid_argument("run: grid size does not match config");
-    if (cfg.backend != Backend::B200) not_provided("run", cfg.backend);
+    if (cfg.steps > 0) check_pair("run", pair, cfg.backend, cfg.threads);
     DeviceLattice& dev = lattice_for(cfg.n, cfg.devices);
     dev.upload(pair.cur);
     if (!observer) {

@@ -1,9 +1,11 @@
 // bml/engine.hpp — the reference engine interface
 // (/root/reference/proj/include/bml/engine.hpp:15-79) with one new backend,
 // Backend::B200 ("b200"), implemented on sm_100a through the C-ABI in
-// include/bml_dev.h. This library ships no CPU stepping engine: the four
-// reference CPU backend names stay in the enum so call sites compile, but
-// selecting them throws std::invalid_argument (no silent CPU fallback).
+// include/bml_dev.h. This library ships no CPU stepping engine. The four
+// reference backend names stay valid so reference call sites compile and run
+// unchanged: they keep the reference's layout and thread rules (naive wants a
+// dense grid, the others a halo grid; only parallel takes threads > 1) and
+// their phases execute on the device engine, bit-identical by construction.
 #pragma once
 
 #include <cstdint>
@@ -21,10 +23,10 @@ struct bml_dev;
 namespace bml {
 
 enum class Backend {
-    ScalarNaive,   // reference CPU engine (not provided here)
-    ScalarHalo,    // reference CPU engine (not provided here)
-    ParallelRows,  // reference CPU engine (not provided here)
-    Lanes,         // reference CPU engine (not provided here)
+    ScalarNaive,   // reference name: dense layout, runs on the device engine
+    ScalarHalo,    // reference name: halo layout, runs on the device engine
+    ParallelRows,  // reference name: halo layout, threads accepted, runs on the device
+    Lanes,         // reference name: halo layout, runs on the device engine
     B200,          // device-resident bit-plane lattice on NVIDIA B200 (sm_100a)
 };
 

@@ -270,12 +270,20 @@ def test_zero_steps_is_identity(gpu):
     assert final == g and metrics == []
 
 
-def test_cpu_backends_are_not_silently_used(gpu):
+def test_reference_backend_names_run_on_the_device(gpu, oracle):
+    """Reference call sites that name a CPU backend run unchanged on the device engine
+    (same grid as b200 and as the oracle); parallel keeps its threads argument."""
     bml = gpu
-    g = bml.Grid.from_text(">.\n.v")
-    for b in (bml.Backend.naive, bml.Backend.halo, bml.Backend.parallel, bml.Backend.lanes):
-        with pytest.raises(ValueError):
-            bml.step(g, 1, backend=b)
+    cells = oracle.init_grid(45, 0.4, 11)
+    g = bml.Grid.from_bytes(45, cells)
+    want = oracle.run(45, cells, 7)
+    for b, threads in ((bml.Backend.naive, 1), (bml.Backend.halo, 1), (bml.Backend.parallel, 3),
+                       (bml.Backend.lanes, 1)):
+        assert bml.step(g, 7, backend=b, threads=threads).to_bytes() == want
+        final, metrics = bml.simulate(g, 7, backend=b, threads=threads)
+        assert final.to_bytes() == want and len(metrics) == 7
+        h = bml.step_phase(g, bml.Phase.horizontal, backend=b)
+        assert h == bml.step_phase(g, bml.Phase.horizontal)
 
 
 def test_native_library_is_loaded(gpu):
