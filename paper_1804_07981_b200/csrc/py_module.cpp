@@ -7,6 +7,7 @@
 #include <pybind11/functional.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
+#include <pybind11/stl/filesystem.h>
 
 #include <cstring>
 #include <stdexcept>
@@ -190,7 +191,8 @@ PYBIND11_MODULE(_bml, m) {
         const auto bytes = bml::encode_ppm(g);
         return py::bytes(reinterpret_cast<const char*>(bytes.data()), bytes.size());
     }, py::arg("grid"));
-    m.def("write_ppm", [](const bml::Grid& g, const std::string& path) { bml::write_ppm(g, path); },
+    // str or os.PathLike, as in the reference binding (py_module.cpp:135)
+    m.def("write_ppm", [](const bml::Grid& g, const std::filesystem::path& path) { bml::write_ppm(g, path); },
           py::arg("grid"), py::arg("path"));
 
     m.def("vehicles_per_species", &bml::vehicles_per_species, py::arg("n"), py::arg("rho"));

@@ -14,6 +14,7 @@ GPU test from the prebuilt binary (the GPU box has no /root/reference).
 """
 import os
 import subprocess
+import sys
 
 import pytest
 
@@ -77,3 +78,35 @@ def test_reference_unit_tests_on_the_device(gpu):
     assert r.returncode == 0, r.stdout + r.stderr
     summary = r.stdout.strip().splitlines()[-1]
     assert ", 0 failed, 0 skipped" in summary, summary
+
+
+# ----------------------------------------------------------- the reference's Python smoke tests
+REF_PY_TESTS = "/root/reference/proj/tests/python/test_smoke.py"
+# cases that step a lattice (need the device); run on a B200 as recorded in
+# profiles/r1_reference_python_smoke_b200.txt
+REF_PY_DEVICE_CASES = "single_step_golden or backends_agree or simulate_metrics or verify_backends"
+
+
+def reference_python_smoke(tmp_dir, select=None):
+    """Run the reference's tests/python/test_smoke.py, unmodified and in place, with
+    `import bml` resolving to this package (a one-line alias package in tmp_dir)."""
+    pkg = os.path.join(tmp_dir, "bml")
+    os.makedirs(pkg, exist_ok=True)
+    with open(os.path.join(pkg, "__init__.py"), "w") as f:
+        f.write("from paper_1804_07981_b200 import *  # noqa: F401,F403\n"
+                "from paper_1804_07981_b200 import __all__, __version__  # noqa: F401\n")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([tmp_dir, ROOT]), PYTHONDONTWRITEBYTECODE="1")
+    env.pop("BML_CLI", None)  # the reference CLI is out of scope (DESIGN.md §8)
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "--rootdir", tmp_dir,
+           REF_PY_TESTS]
+    if select:
+        cmd += ["-k", select]
+    return subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=tmp_dir, timeout=600)
+
+
+def test_reference_python_smoke_host_cases(tmp_path):
+    if not os.path.exists(REF_PY_TESTS):
+        pytest.skip("reference sources not present on this host")
+    r = reference_python_smoke(str(tmp_path), select=f"not ({REF_PY_DEVICE_CASES})")
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "4 passed" in r.stdout, r.stdout
