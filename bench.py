@@ -35,6 +35,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+DATASHEET_HBM_GBS = 8000.0  # B200 datasheet HBM3e bandwidth per GPU
 
 WORKLOADS = {
     # name: (n, rho, seed, steps, description)
@@ -375,6 +376,7 @@ def run_b200(args, wl):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": kernel, "peak_source": peak_src,
+                     "frac_datasheet": achieved / DATASHEET_HBM_GBS,  # also vs 8 TB/s
                      "launch_geometry": last_launch(abi, h) if kernel == "step_block_kernel" else None,
                      "resident_cluster": lat.resident_cluster,
                      "algorithmic_bytes_per_cell_update": BYTES_PER_CELL_UPDATE,
@@ -533,6 +535,7 @@ def run_b200_multi(args, wl):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "step_block_kernel",
                          "peak_source": peak_src, "launches_per_rank": launches,
+                         "frac_datasheet": achieved / DATASHEET_HBM_GBS,  # per rank, like frac
                          "avg_launch_us": avg_launch_ms * 1e3},
             "cpu_baseline": None,
             "e2e": {"value": n * n * steps * args.steps / float(et[0]) / 1e9, "unit": "Gcell-updates/s",
