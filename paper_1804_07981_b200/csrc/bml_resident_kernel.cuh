@@ -88,7 +88,10 @@ struct ResidentArgs {
 
 constexpr int kResidentMaxWarps = 32;
 constexpr int kResidentMaxGhost = 16;
-constexpr int kResidentGhost = 8;  // default ghost depth G (bml_dev.cu resident_plan)
+#ifndef BML_RESIDENT_GHOST
+#define BML_RESIDENT_GHOST 8
+#endif
+constexpr int kResidentGhost = BML_RESIDENT_GHOST;  // default ghost depth G (bml_dev.cu resident_plan)
 
 // PACK: rows per register. A lattice narrower than a warp (W = 32 / PACK words,
 // n = 256 -> PACK 4) packs PACK rows into the 32 lanes: lane = segment * W +
