@@ -67,3 +67,44 @@ def test_random_configuration_matches_oracle(gpu, oracle, case):
         want = oracle.run(n, cells, steps)
     assert lat.download().to_bytes() == want
     assert lat.digest() == oracle.digest(n, want)
+
+
+def _band_cases():
+    rng = random.Random(FUZZ_SEED + 1)
+    out = []
+    while len(out) < 32:
+        n = rng.choice([rng.randint(64, 700), 32 * rng.randint(2, 40), rng.randint(993, 1400)])
+        devices = rng.randint(2, 4)
+        if n - (devices - 1) * ((n + devices - 1) // devices) < 16:  # engine.cpp band split rule
+            continue
+        rho = round(rng.uniform(0.2, 0.6), 4)
+        steps = rng.randint(1, 120)
+        block = rng.choice([1, 2, 4, 8, 16, 16])
+        strip = rng.choice([0, 0, rng.randint(16, 200)])  # connected bands: strips >= 16 rows
+        metrics = rng.random() < 0.5
+        out.append((len(out), n, devices, rho, steps, block, strip, metrics, rng.getrandbits(32)))
+    return out
+
+
+@pytest.mark.parametrize("case", _band_cases(), ids=lambda c: f"b{c[0]}_n{c[1]}_d{c[2]}_s{c[4]}_b{c[5]}")
+def test_random_row_bands_match_oracle(gpu, oracle, case):
+    """Row bands exchanging ghost rows inside the step kernel, all
+    placed on the one visible GPU: same lattice, counters and digest as one band."""
+    bml = gpu
+    _, n, devices, rho, steps, block, strip, metrics, seed = case
+    cells = oracle.init_grid(n, rho, seed)
+    lat = bml.DeviceLattice(n, devices)
+    lat.configure(block_steps=block, strip_rows=strip)
+    lat.upload(bml.Grid.from_bytes(n, cells))
+    if metrics:
+        got = lat.step_with_metrics(steps)
+        want, (lm, tm, lc, tc) = oracle.run(n, cells, steps, metrics=True)
+        assert [m.lr_moved for m in got] == lm
+        assert [m.tb_moved for m in got] == tm
+        assert [m.lr_count for m in got] == lc
+        assert [m.tb_count for m in got] == tc
+    else:
+        lat.step(steps)
+        want = oracle.run(n, cells, steps)
+    assert lat.download().to_bytes() == want
+    assert lat.digest() == oracle.digest(n, want)
