@@ -190,8 +190,11 @@ def reference_arm(n, rho, seed, steps, reps):
     lanes_steps, par_steps = cpu_sample_plan(n, steps)
     lanes = ref_bench(n, rho, seed, lanes_steps, "lanes", 1, reps)
     par = ref_bench(n, rho, seed, par_steps, "parallel", 0, reps)
+    # the paper's scalar ladder: ~1 s samples, one rep each
+    halo = ref_bench(n, rho, seed, max(1, min(steps, int(1.5e8 / (n * n)))), "halo", 1, 1)
+    naive = ref_bench(n, rho, seed, max(1, min(steps, int(0.8e8 / (n * n)))), "naive", 1, 1)
     best = lanes if lanes["gcups"] >= par["gcups"] else par
-    return {"lanes": lanes, "parallel": par, "best": best}, None
+    return {"lanes": lanes, "parallel": par, "halo": halo, "naive": naive, "best": best}, None
 
 
 def cpu_model():
@@ -241,6 +244,8 @@ def run_reference_impl(args, wl):
             "lane_width": best["lane_width"],
             "lanes_1thread_gcups": res["lanes"]["gcups"],
             "parallel_all_threads_gcups": res["parallel"]["gcups"],
+            "halo_1thread_gcups": res["halo"]["gcups"],
+            "naive_1thread_gcups": res["naive"]["gcups"],
             "parallel_threads": res["parallel"]["threads"],
         },
         "e2e": {"value": value, "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
@@ -352,6 +357,10 @@ def run_b200(args, wl):
                    "host": cpu_model(),
                    "lanes_1thread_gcups": res["lanes"]["gcups"],
                    "parallel_all_threads_gcups": res["parallel"]["gcups"],
+                   "halo_1thread_gcups": res["halo"]["gcups"],
+                   "naive_1thread_gcups": res["naive"]["gcups"],
+            "halo_1thread_gcups": res["halo"]["gcups"],
+            "naive_1thread_gcups": res["naive"]["gcups"],
                    "parallel_threads": res["parallel"]["threads"]}
         else:
             cpu = {"value": None, "unavailable": err}
