@@ -9,7 +9,7 @@ import time
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-lib = ctypes.CDLL(os.path.join(ROOT, "paper_1804_07981_b200", "libbml_dev.so"))
+lib = ctypes.CDLL(os.environ.get("BML_LIB", os.path.join(ROOT, "paper_1804_07981_b200", "libbml_dev.so")))
 vp = ctypes.c_void_p
 lib.bml_dev_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
 lib.bml_dev_upload.argtypes = [vp, vp, ctypes.c_size_t]
