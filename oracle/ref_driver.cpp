@@ -25,6 +25,7 @@
 //   ref_driver info
 // Lattice files are the n*n interior bytes, row-major (values 0/1/2).
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -157,6 +158,14 @@ int simulate_and_report(const bml::Grid& initial, const Args& a, long steps, dou
                           static_cast<long long>(m.step), static_cast<long long>(m.lr_count),
                           static_cast<long long>(m.tb_count), static_cast<long long>(m.lr_moved),
                           static_cast<long long>(m.tb_moved), m.mobility);
+            metrics_json += buf;
+            // the regime the reference's CLI / acceptance program reports: classify()
+            // over the last kClassifyWindow mobilities (acceptance_main.cpp:74-78)
+            const std::size_t w = std::min(all.size(), static_cast<std::size_t>(bml::kClassifyWindow));
+            std::vector<double> window;
+            for (std::size_t i = all.size() - w; i < all.size(); ++i) window.push_back(all[i].mobility);
+            std::snprintf(buf, sizeof buf, ",\"regime\":\"%s\"",
+                          std::string(bml::regime_name(bml::classify(window))).c_str());
             metrics_json += buf;
         }
         const std::string per_step = get(a, "per_step", "");

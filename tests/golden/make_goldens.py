@@ -10,6 +10,7 @@ GPU box (which has no /root/reference) can check the CUDA path against it.
     python tests/golden/make_goldens.py c3         # N=32768 only (~95 min, lanes)
     python tests/golden/make_goldens.py c4short    # N=65536, 1000 steps (~45 min, 43 GB RAM)
     python tests/golden/make_goldens.py c4         # N=65536, 10000 steps (~6 h, 43 GB RAM)
+    python tests/golden/make_goldens.py regimes    # N=256, rho .25/.38, seeds 1-10, 4096 steps (~1 min)
 
 Every record holds the reference's init digest, final digest after `steps`
 full steps, the vehicle counts and (where metrics=1) the observer-path sums
@@ -64,8 +65,33 @@ def run(c, force=False):
     print("wrote", out, rec["final_digest"], flush=True)
 
 
+# Phase-transition regimes (acceptance_main.cpp criteria 3/4):
+# N=256, 4096 steps, seeds 1..10 at the free-flow and jamming densities. One
+# combined file (not ref_*.json: those are single records).
+REGIMES = [dict(n=256, rho=rho, seed=s, steps=4096, metrics=1) for rho in (0.25, 0.38)
+           for s in range(1, 11)]
+
+
+def run_regimes():
+    out = os.path.join(HERE, "regimes_n256_steps4096.json")
+    recs = []
+    for c in REGIMES:
+        args = [DRIVER, "golden"] + [f"{k}={v}" for k, v in c.items()] + ["backend=lanes"]
+        print("running", " ".join(args), flush=True)
+        r = json.loads(subprocess.run(args, check=True, capture_output=True, text=True).stdout)
+        recs.append({k: r[k] for k in ("n", "rho", "seed", "steps", "init_digest", "final_digest",
+                                       "sum_lr_moved", "sum_tb_moved", "regime")})
+    with open(out, "w") as f:
+        json.dump({"generator": "oracle/_ref/ref_driver (unmodified reference sources, lanes backend)",
+                   "window": 64, "records": recs}, f, indent=1, sort_keys=True)
+    print("wrote", out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "small"
+    if which == "regimes":
+        run_regimes()
+        sys.exit(0)
     c4short = [dict(n=65536, rho=0.35, seed=1, steps=1000, metrics=0)]
     table = {"small": SMALL, "big": BIG, "huge": HUGE, "c3": HUGE[:1], "c4short": c4short,
              "c4": HUGE[1:]}[which]
