@@ -6,7 +6,18 @@ reference. 1 cell-update = one cell advanced by one full BML step (LR + TB phase
 
 A bench "step" = one reference-style run(): `steps` full BML steps of the whole
 N x N lattice (the unit the reference's own `bml bench` times, tools/main.cpp:195-201).
-Default workload = BASELINE configs[1]: N=1024, rho=0.38, 4096 steps, seed 1.
+Default workload = BASELINE configs[4], the metric's configuration: N=65536 (4 Gi
+cells), rho=0.35, 10000 steps, seed 1. With --gpus g (torchrun, one rank per GPU) the
+lattice is split into row bands of ceil(N/g) rows (the reference's only parallel
+split, engine.cpp:131-137):
+  --scaling strong (default)  N fixed: the literal configs[3]/[4] 1/2/4/8 sweep
+  --scaling weak              configs[4]: the square weak sweep N = 23168 / 32768 /
+                              46336 / 65536 at g = 1 / 2 / 4 / 8 (SURVEY §8(d) item 5);
+                              other workloads: ~g x the N=1 cells, side a multiple of 32
+  parity    untimed, after the timed region: the lattice re-drawn from the reference
+            RNG path and run for the golden's step count on the device; its grid_digest
+            must equal the digest the UNMODIFIED reference produced
+            (tests/golden/ref_*.json), and so must the e2e leg's downloaded result.
 
   value     device-resident throughput: lattice already in HBM, CUDA events on the
             launching stream around each bench step, L2 flushed (256 MiB write)
@@ -17,15 +28,21 @@ Default workload = BASELINE configs[1]: N=1024, rho=0.38, 4096 steps, seed 1.
             cell-update / its average launch time, vs the
             measured HBM copy bandwidth in MEASURED_PEAKS.json.
   cpu_baseline  the unmodified reference (oracle/_ref/ref_driver, its own bench
-            method) on this host, bounded sample, rank 0 only.
+            method) on this host, bounded sample, rank 0 only. From N=4096 up it
+            steps the device-drawn input lattice (digest-checked against the
+            reference's own init digest) instead of repeating the reference's
+            minutes-long init_grid.
 
 --impl reference runs only the reference CPU implementation (best of `lanes` 1
-thread and `parallel` with all host threads) and prints the same line shape.
+thread and `parallel` with all host threads, after ONE reference init_grid) and
+prints the same line shape.
 """
 import argparse
 import ctypes
 import json
+import math
 import os
+import tempfile
 import statistics
 import subprocess
 import sys
@@ -48,6 +65,41 @@ WORKLOADS = {
 }
 DEVICE_INIT_N = 4096  # init_grid on the device from this side up (minutes on the host at 65536)
 BYTES_PER_CELL_UPDATE = 4  # 1 B read + 1 B write per cell per phase
+SQUARE_WEAK = {1: 23168, 2: 32768, 4: 46336, 8: 65536}  # SURVEY §8(d) item 5 (configs[4])
+GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
+
+
+def bench_n(workload, n1, world, scaling):
+    """Lattice side for `world` ranks: fixed (strong) or the weak-scaling sweep."""
+    if scaling == "strong" or world < 1:
+        return n1
+    if workload == "c4":
+        if world in SQUARE_WEAK:
+            return SQUARE_WEAK[world]
+        return min(65536, int(round(23168 * math.sqrt(world) / 32.0)) * 32)
+    from paper_1804_07981_b200.dist import weak_scaled_n
+
+    return weak_scaled_n(n1, world)
+
+
+def find_golden(n, rho, seed, steps):
+    """The reference's own digests for (n, rho, seed): the record at `steps` if one
+    is committed, else the longest one (None if there is none)."""
+    best = None
+    prefix = f"ref_n{n}_rho{rho}_seed{seed}_steps"
+    if not os.path.isdir(GOLDEN_DIR):
+        return None
+    for name in os.listdir(GOLDEN_DIR):
+        if not (name.startswith(prefix) and name.endswith(".json")):
+            continue
+        with open(os.path.join(GOLDEN_DIR, name)) as f:
+            rec = json.load(f)
+        rec["file"] = "tests/golden/" + name
+        if rec["steps"] == steps:
+            return rec
+        if best is None or rec["steps"] > best["steps"]:
+            best = rec
+    return best
 
 
 def measured_peaks():
@@ -151,15 +203,6 @@ def abi_check(lib, rc, what):
 
 
 # ---------------------------------------------------------------- reference CPU arm
-def ref_bench(n, rho, seed, steps, backend, threads, reps):
-    out = subprocess.run([REF_DRIVER, "bench", f"n={n}", f"rho={rho}", f"seed={seed}",
-                          f"steps={steps}", f"backend={backend}", f"threads={threads}",
-                          f"reps={reps}"], check=True, capture_output=True, text=True)
-    rec = json.loads(out.stdout)
-    rec["gcups"] = n * n * steps / rec["mean_s"] / 1e9
-    return rec
-
-
 def alu_roofline(kernel, achieved_gcups, resident_cluster, sm_max_mhz, sms=148):
     """The bound that actually limits the bit-plane kernels: the
     ALU pipe. Per 32-cell stage the kernels issue 6 ALU-pipe instructions (4 LOP3
@@ -176,25 +219,61 @@ def alu_roofline(kernel, achieved_gcups, resident_cluster, sm_max_mhz, sms=148):
             "alu_instructions_per_32_cell_stage": 6}
 
 
-def cpu_sample_plan(n, steps):
-    """Bounded samples (~seconds each) of the same workload for the CPU arms."""
+def cpu_sample_plan(n, steps, reps):
+    """Bounded samples of the same workload for the reference CPU backends, as
+    ref_driver `ladder` plan items backend:threads:steps:reps. lanes (1 thread, the
+    reference's fastest path) gets `reps` reps of ~1-3 s; parallel (all host threads,
+    scalar kernel) up to 3 reps; the paper's scalar ladder (halo, naive) one rep."""
     cells = n * n
-    lanes_steps = max(1, min(steps, int(6e9 / cells)))      # ~1-3 s at 2-6 Gcell/s
-    par_steps = max(1, min(steps, int(1.5e9 / cells)))      # scalar kernel, all threads
-    return lanes_steps, par_steps
+    lanes_steps = max(1, min(steps, int(6e9 / cells)))
+    par_steps = max(1, min(steps, int(1.5e9 / cells)))
+    halo_steps = max(1, min(steps, int(1.5e8 / cells)))
+    naive_steps = max(1, min(steps, int(0.8e8 / cells)))
+    return [("lanes", 1, lanes_steps, reps), ("parallel", 0, par_steps, min(reps, 3)),
+            ("halo", 1, halo_steps, 1), ("naive", 1, naive_steps, 1)]
 
 
-def reference_arm(n, rho, seed, steps, reps):
+def reference_ladder(n, rho, seed, steps, reps, input_path=None, expect_init=None):
+    """ONE ref_driver process: one input lattice (the reference's own init_grid, or a
+    digest-checked file), then the reference bench method per backend."""
     if not os.path.exists(REF_DRIVER):
         return None, "oracle/_ref/ref_driver not built"
-    lanes_steps, par_steps = cpu_sample_plan(n, steps)
-    lanes = ref_bench(n, rho, seed, lanes_steps, "lanes", 1, reps)
-    par = ref_bench(n, rho, seed, par_steps, "parallel", 0, reps)
-    # the paper's scalar ladder (SURVEY §8(d)): ~1 s samples, one rep each
-    halo = ref_bench(n, rho, seed, max(1, min(steps, int(1.5e8 / (n * n)))), "halo", 1, 1)
-    naive = ref_bench(n, rho, seed, max(1, min(steps, int(0.8e8 / (n * n)))), "naive", 1, 1)
-    best = lanes if lanes["gcups"] >= par["gcups"] else par
-    return {"lanes": lanes, "parallel": par, "halo": halo, "naive": naive, "best": best}, None
+    plan = ",".join(f"{b}:{t}:{st}:{r}" for b, t, st, r in cpu_sample_plan(n, steps, reps))
+    cmd = [REF_DRIVER, "ladder", f"n={n}", f"rho={rho}", f"seed={seed}", f"plan={plan}"]
+    if input_path:
+        cmd.append(f"in={input_path}")
+        if expect_init:
+            cmd.append(f"expect_init={expect_init}")
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        return None, f"ref_driver ladder rc={out.returncode}: {out.stderr.strip()[:200]}"
+    rec = json.loads(out.stdout)
+    res = {}
+    for r in rec["results"]:
+        r["gcups"] = n * n * r["steps"] / r["mean_s"] / 1e9
+        res[r["backend"]] = r
+    res["best"] = res["lanes"] if res["lanes"]["gcups"] >= res["parallel"]["gcups"] else res["parallel"]
+    res["input"] = {"source": rec["init_source"], "init_s": rec["init_s"], "digest": rec["init_digest"]}
+    return res, None
+
+
+def cpu_baseline_record(res, steps, reps):
+    best = res["best"]
+    inp = res["input"]
+    where = ("reference init_grid" if inp["source"] == "init_grid" else
+             "device-drawn input lattice, grid_digest checked equal to the reference init digest")
+    return {"value": best["gcups"], "unit": "Gcell-updates/s", "cores": best["threads"],
+            "kind": "reference",
+            "sample": (f"{best['backend']} backend, {best['steps']} of {steps} steps x {best['reps']} reps, "
+                       f"reference bench method (tools/main.cpp:195-214); input: {where}"),
+            "host": cpu_model(), "hardware_concurrency": best["hardware_concurrency"],
+            "lane_width": best["lane_width"],
+            "lanes_1thread_gcups": res["lanes"]["gcups"],
+            "parallel_all_threads_gcups": res["parallel"]["gcups"],
+            "halo_1thread_gcups": res["halo"]["gcups"],
+            "naive_1thread_gcups": res["naive"]["gcups"],
+            "parallel_threads": res["parallel"]["threads"],
+            "input_init_s": inp["init_s"], "input_digest": inp["digest"]}
 
 
 def cpu_model():
@@ -209,17 +288,20 @@ def cpu_model():
 
 
 def run_reference_impl(args, wl):
-    n, rho, seed, steps, desc = wl
+    n1, rho, seed, steps, desc = wl
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
+    n = bench_n(args.workload, n1, max(world, args.gpus), args.scaling)
     reps = max(1, args.steps)
-    res, err = reference_arm(n, rho, seed, steps, reps)
+    res, err = reference_ladder(n, rho, seed, steps, reps)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": err}))
         return
     best = res["best"]
     value = best["gcups"]
+    golden = find_golden(n, rho, seed, steps)
     line = {
         "impl": "reference",
         "metric": "Gcell-updates/sec",
@@ -230,28 +312,30 @@ def run_reference_impl(args, wl):
         "warmup": 0,
         "ms_per_step": best["mean_s"] * 1e3 * steps / best["steps"],
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic (reference init_grid seed)",
-        "config": {"workload": desc, "n": n, "rho": rho, "seed": seed, "steps_per_run": steps},
-        "cpu_baseline": {
-            "value": value, "unit": "Gcell-updates/s", "cores": best["threads"],
-            "kind": "reference",
-            "sample": (f"{best['backend']} backend, {best['steps']} of {steps} steps per rep, "
-                       f"{reps} reps, reference bench method (tools/main.cpp:195-214)"),
-            "host": cpu_model(), "hardware_concurrency": best["hardware_concurrency"],
-            "lane_width": best["lane_width"],
-            "lanes_1thread_gcups": res["lanes"]["gcups"],
-            "parallel_all_threads_gcups": res["parallel"]["gcups"],
-            "halo_1thread_gcups": res["halo"]["gcups"],
-            "naive_1thread_gcups": res["naive"]["gcups"],
-            "parallel_threads": res["parallel"]["threads"],
-        },
+        "config": config_block(args, desc, n, rho, seed, steps, args.gpus),
+        "cpu_baseline": cpu_baseline_record(res, steps, reps),
         "e2e": {"value": value, "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "input_check": {"init_digest": res["input"]["digest"],
+                        "golden_init_digest": golden["init_digest"] if golden else None,
+                        "match": (res["input"]["digest"] == golden["init_digest"]) if golden else None},
     }
     print(json.dumps(line))
+
+
+def config_block(args, desc, n, rho, seed, steps, world):
+    wl = desc if n == WORKLOADS[args.workload][0] else desc + f" ({args.scaling}-scaled to N={n})"
+    return {"workload": wl, "n": n, "rho": rho, "seed": seed, "steps_per_run": steps,
+            "scaling_mode": args.scaling,
+            "parallelism": "single GPU" if world == 1 else
+            f"row bands of ceil(N/{world}) rows x{world}, NVLink peer ghost rows",
+            "l2": "flushed (256 MiB write) between bench steps",
+            "block_steps": args.block, "strip_rows": args.strip,
+            "layout": "bit-planes, 2 bits/cell"}
 
 
 # ---------------------------------------------------------------- b200 arm
@@ -259,12 +343,13 @@ def run_b200(args, wl):
     import torch
     import paper_1804_07981_b200 as bml
 
-    n, rho, seed, steps, desc = wl
+    n1, rho, seed, steps, desc = wl
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         return run_b200_multi(args, wl)
+    n = bench_n(args.workload, n1, 1, args.scaling)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
@@ -333,37 +418,27 @@ def run_b200(args, wl):
     kernel = "resident_kernel" if lat.resident_cluster > 0 else "step_block_kernel"
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and n == n1:
         with open(tpath) as f:
             t = json.load(f)
         if t.get("kernel", "").startswith(kernel):
             traffic = t.get("dram_bytes_per_launch")
             traffic_src = t.get("source")
 
+    # parity (untimed): the lattice re-drawn from the reference RNG path on the
+    # device, run for the golden's step count, digested on the device
+    golden = find_golden(n, rho, seed, steps)
+    parity = parity_check(bml, lat, n, rho, seed, golden)
+
     # e2e through the C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(abi, torch, bml, grid, n, steps, args)
+        e2e = run_e2e(abi, torch, bml, grid, n, steps, args, golden)
 
     cpu = None
     if not args.no_cpu and rank == 0:
-        res, err = reference_arm(n, rho, seed, steps, 3)
-        if res:
-            best = res["best"]
-            cpu = {"value": best["gcups"], "unit": "Gcell-updates/s", "cores": best["threads"],
-                   "kind": "reference",
-                   "sample": (f"{best['backend']} backend, {best['steps']} of {steps} steps x 3 reps, "
-                              "reference bench method (tools/main.cpp:195-214)"),
-                   "host": cpu_model(),
-                   "lanes_1thread_gcups": res["lanes"]["gcups"],
-                   "parallel_all_threads_gcups": res["parallel"]["gcups"],
-                   "halo_1thread_gcups": res["halo"]["gcups"],
-                   "naive_1thread_gcups": res["naive"]["gcups"],
-            "halo_1thread_gcups": res["halo"]["gcups"],
-            "naive_1thread_gcups": res["naive"]["gcups"],
-                   "parallel_threads": res["parallel"]["threads"]}
-        else:
-            cpu = {"value": None, "unavailable": err}
+        cpu = cpu_baseline_b200_arm(grid, n, rho, seed, steps, golden)
+    del grid
 
     line = {
         "metric": "Gcell-updates/sec",
@@ -374,18 +449,17 @@ def run_b200(args, wl):
         "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic: reference init_grid(n, rho, seed) lattice",
-        "config": {"workload": desc, "n": n, "rho": rho, "seed": seed, "steps_per_run": steps,
-                   "parallelism": "single GPU", "l2": "flushed (256 MiB write) between bench steps",
-                   "block_steps": args.block, "strip_rows": args.strip,
-                   "layout": "bit-planes, 2 bits/cell"},
+        "config": config_block(args, desc, n, rho, seed, steps, 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": kernel, "peak_source": peak_src,
                      "frac_datasheet": achieved / DATASHEET_HBM_GBS,  # also vs 8 TB/s
+                     "binding_bound": "alu (see roofline_alu): temporal blocking keeps DRAM traffic "
+                                      "at ~1/16 of the 4 B/cell-update algorithmic figure",
                      "launch_geometry": last_launch(abi, h) if kernel == "step_block_kernel" else None,
                      "resident_cluster": lat.resident_cluster,
                      "algorithmic_bytes_per_cell_update": BYTES_PER_CELL_UPDATE,
@@ -395,6 +469,7 @@ def run_b200(args, wl):
                                      lat.resident_cluster, clocks.summary().get("sm_max_mhz")),
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "parity": parity,
         "gpu_launches": timed_launches,
         "init": {"s": t_init, "where": "device" if n >= DEVICE_INIT_N else "host",
                  "note": "init_grid incl. readback into a host Grid; untimed input generation"},
@@ -405,7 +480,41 @@ def run_b200(args, wl):
     print(json.dumps(line))
 
 
-def run_e2e(abi, torch, bml, grid, n, steps, args):
+def parity_check(bml, lat, n, rho, seed, golden):
+    """Device digest after an untimed re-draw + golden-length run vs the reference's."""
+    if golden is None:
+        return {"golden": None, "match": None, "note": f"no reference golden committed for n={n}"}
+    lat.init_random(rho, seed)
+    init_d = lat.digest()
+    lat.step(golden["steps"])
+    final_d = lat.digest()
+    ok = (f"0x{init_d:016x}" == golden["init_digest"] and f"0x{final_d:016x}" == golden["final_digest"])
+    return {"golden": golden["file"], "steps": golden["steps"], "init_digest": f"0x{init_d:016x}",
+            "final_digest": f"0x{final_d:016x}", "expected_final": golden["final_digest"], "match": ok}
+
+
+def cpu_baseline_b200_arm(grid, n, rho, seed, steps, golden):
+    """Reference CPU sample for this line (rank 0, N=1). Large lattices hand the
+    reference the device-drawn input (checked against the reference init digest)
+    rather than a second minutes-long host init_grid."""
+    path = None
+    try:
+        expect = None
+        if n >= DEVICE_INIT_N:
+            fd, path = tempfile.mkstemp(prefix="bml_in_", suffix=".bin")
+            with os.fdopen(fd, "wb") as f:
+                f.write(grid.to_bytes())
+            expect = golden["init_digest"] if golden else f"0x{grid.digest():016x}"
+        res, err = reference_ladder(n, rho, seed, steps, 3, input_path=path, expect_init=expect)
+    finally:
+        if path:
+            os.unlink(path)
+    if not res:
+        return {"value": None, "unavailable": err}
+    return cpu_baseline_record(res, steps, 3)
+
+
+def run_e2e(abi, torch, bml, grid, n, steps, args, golden):
     vp = ctypes.c_void_p
     h = vp()
     abi_check(abi, abi.bml_dev_create(n, torch.cuda.current_device(), ctypes.byref(h)), "create")
@@ -424,28 +533,34 @@ def run_e2e(abi, torch, bml, grid, n, steps, args):
             abi_check(abi, abi.bml_dev_step(h, steps, None, None, None, None), "step")
             abi_check(abi, abi.bml_dev_download(h, vp(host_out.data_ptr()), n), "download")
             times.append(time.perf_counter() - t0)
-        # correctness of what was timed: the device result equals the public API's
-        final = bml.step(grid, steps)
-        assert bytes(host_out.numpy()) == final.to_bytes(), "e2e result mismatch"
+        # what was timed is checked against the UNMODIFIED reference: the downloaded
+        # lattice's host grid_digest equals the golden (when one exists at `steps`)
+        check = None
+        if golden is not None and golden["steps"] == steps:
+            d = bml.Grid.from_bytes(n, bytes(host_out.numpy())).digest()
+            check = {"golden": golden["file"], "digest": f"0x{d:016x}",
+                     "match": f"0x{d:016x}" == golden["final_digest"]}
+            assert check["match"], f"e2e result differs from the reference golden: {check}"
         total = sum(times)
         return {"value": n * n * steps * len(times) / total / 1e9, "unit": "Gcell-updates/s",
                 "h2d_bytes_per_step": n * n, "d2h_bytes_per_step": n * n,
                 "ms_per_step": total / len(times) * 1e3,
-                "path": "C-ABI bml_dev_upload/step/download, pinned host buffers"}
+                "path": "C-ABI bml_dev_upload/step/download, pinned host buffers",
+                "result_check": check}
     finally:
         abi.bml_dev_destroy(h)
 
 
 def run_b200_multi(args, wl):
-    """One process per GPU (torchrun): each rank owns a row band of a weak-scaled
-    square lattice (~world x the cells of the N=1 workload, side a multiple of 32);
-    neighbours exchange ghost rows inside the step kernel over NVLink (CUDA IPC
-    peer stores + flags). torch.distributed only bootstraps and reduces timings."""
+    """One process per GPU (torchrun): each rank owns a row band of ceil(N/g) rows of
+    the lattice (N fixed for --scaling strong, the square weak sweep for weak);
+    neighbours exchange ghost rows inside the step kernel over NVLink (CUDA IPC peer
+    stores + flags). torch.distributed only bootstraps and reduces timings."""
     import torch
     import torch.distributed as dist
 
     import paper_1804_07981_b200 as bml
-    from paper_1804_07981_b200.dist import BandLattice, combine_digest, weak_scaled_n
+    from paper_1804_07981_b200.dist import BandLattice, combine_digest
 
     n1, rho, seed, steps, desc = wl
     rank = int(os.environ["RANK"])
@@ -461,10 +576,15 @@ def run_b200_multi(args, wl):
     else:
         dist.init_process_group("nccl", device_id=dev)
     red_dev = torch.device("cpu") if shared_gpu else dev
-    n = weak_scaled_n(n1, world)
+    n = bench_n(args.workload, n1, world, args.scaling)
     band = BandLattice(n, rank, world, local, block_steps=args.block, strip_rows=args.strip)
-    # each rank draws its rows of the same reference-RNG lattice on its own GPU
-    band.init_random(rho, seed)
+    # each rank draws its rows of the same reference-RNG lattice on its own GPU; ranks
+    # sharing one GPU take turns (the draw needs ~16 B per cell of scratch)
+    for turn in range(world if shared_gpu else 1):
+        if not shared_gpu or turn == rank:
+            band.init_random(rho, seed)
+        if shared_gpu:
+            dist.barrier()
     band.exchange_halos()
     band_cells = band.download_rows()  # host copy of the input, for the e2e leg
     stream = torch.cuda.Stream(device=dev)
@@ -530,30 +650,33 @@ def run_b200_multi(args, wl):
     k_total = sum(lr for _, _, (lr, _) in segs), sum(tb for _, _, (_, tb) in segs)
     conserved = k_total == (bml.vehicles_per_species(n, rho),) * 2
     if rank == 0:
+        golden = find_golden(n, rho, seed, steps)
+        match = None
+        if golden is not None and golden["steps"] == steps:
+            match = f"0x{digest:016x}" == golden["final_digest"]
         line = {
             "metric": "Gcell-updates/sec", "value": value, "unit": "Gcell-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u8",
             "data": "synthetic: reference init_grid(n, rho, seed) lattice",
-            "config": {"workload": desc + f" weak-scaled to n={n}", "n": n, "rho": rho, "seed": seed,
-                       "steps_per_run": steps, "parallelism": f"row bands x{world}, NVLink peer ghost rows",
-                       "l2": "flushed (256 MiB write) between bench steps",
-                       "block_steps": args.block, "layout": "bit-planes, 2 bits/cell",
-                       "shared_gpu": shared_gpu},
+            "config": dict(config_block(args, desc, n, rho, seed, steps, world), shared_gpu=shared_gpu),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "step_block_kernel",
                          "peak_source": peak_src, "launches_per_rank": launches,
                          "frac_datasheet": achieved / DATASHEET_HBM_GBS,  # per rank, like frac
+                         "binding_bound": "alu (per rank; see the N=1 line's roofline_alu)",
                          "avg_launch_us": avg_launch_ms * 1e3},
             "cpu_baseline": None,
             "e2e": {"value": n * n * steps * args.steps / float(et[0]) / 1e9, "unit": "Gcell-updates/s",
                     "h2d_bytes_per_step": n * n, "d2h_bytes_per_step": n * n},
             "gpu_launches": timed_launches * world, "wall_s": wall, "clocks": clocks.summary(),
-            "final": {"digest": f"0x{digest:016x}", "vehicles": list(k_total), "conserved": conserved,
-                      "steps": steps,
-                      "note": "grid_digest of init_grid(n, rho, seed) after `steps` steps (the last e2e "
-                              "run), combined on rank 0 from the bands' device digest segments"},
+            "parity": {"digest": f"0x{digest:016x}", "vehicles": list(k_total), "conserved": conserved,
+                       "steps": steps, "golden": golden["file"] if golden else None,
+                       "expected_final": golden["final_digest"] if golden and golden["steps"] == steps
+                       else None, "match": match,
+                       "note": "grid_digest of init_grid(n, rho, seed) after `steps` steps (the last e2e "
+                               "run), combined on rank 0 from the bands' device digest segments"},
         }
         print(json.dumps(line))
     band.close()
@@ -566,7 +689,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c1")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="N>1: fixed N split into row bands (strong) or the weak sweep")
     ap.add_argument("--block", type=int, default=16, help="steps fused per launch / resident ghost depth")
     ap.add_argument("--strip", type=int, default=0, help="streaming-kernel rows per strip (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -100,12 +100,19 @@ int bml_dev_phase(bml_dev *dev, int phase, int64_t *moved);
  * arrays is nullable; when any is non-NULL, all requested arrays (length
  * `steps`) receive the per-step values of the reference observer loop
  * (engine.cpp:211-235): lr_moved, tb_moved, and the post-step lr/tb counts.
- * The moved counts are popcounts fused into the step kernels. For a whole torus
- * (single band) the rules conserve both species exactly, so the per-step counts
- * are the counts measured before the run, and the final lattice is re-counted:
- * any difference returns BML_ECONSERVE (engine.cpp:219-224's check). For row
- * bands, whose counts change as TB vehicles cross band edges, the kernels count
- * every step and the values are this band's share. */
+ * The moved counts are popcounts fused into the step kernels. The vehicle
+ * census (count_vehicles after a step, engine.cpp:219-224) is measured inside
+ * the kernels too:
+ *   - row bands (counts change as TB vehicles cross band edges), the
+ *     cluster-resident small-lattice kernel, and strict mode
+ *     (bml_dev_set_census(dev, 1)): after EVERY step;
+ *   - otherwise (single band, streaming kernel): after the last step of every
+ *     launch (every <= 16 steps); in between, the last measured count.
+ * A single band checks every measured census against the counts before the
+ * run. On a difference the arrays are still filled (through the violating
+ * step) and BML_ECONSERVE is returned; the message names the first step, 1-based
+ * within this call, whose census differs — the exact step the reference would
+ * throw at when the census is per step, else the launch boundary that saw it. */
 int bml_dev_step(bml_dev *dev, int64_t steps, int64_t *lr_moved, int64_t *tb_moved,
                  int64_t *lr_count, int64_t *tb_count);
 
@@ -128,8 +135,9 @@ int bml_dev_encode_ppm(bml_dev *dev, uint8_t *dst, size_t dst_pitch);
 int bml_dev_counts(bml_dev *dev, int64_t *lr, int64_t *tb);
 
 /* Launch on an external CUDA stream (cudaStream_t passed as void*; NULL
- * restores the handle's own stream). Used by bench.py to time on the launching
- * stream with CUDA events. */
+ * restores the handle's own stream). Work already queued on the previous stream
+ * is ordered before anything queued on the new one (event + stream wait). Used
+ * by bench.py to time on the launching stream with CUDA events. */
 int bml_dev_set_stream(bml_dev *dev, void *stream);
 int bml_dev_sync(bml_dev *dev);
 
@@ -147,6 +155,19 @@ int bml_dev_configure(bml_dev *dev, int block_steps, int strip_rows);
  * last bml_dev_step (0 = streaming kernel). */
 int bml_dev_set_resident(bml_dev *dev, int mode);
 int bml_dev_path(bml_dev *dev, int *resident_cluster);
+
+/* Census cadence of bml_dev_step's vehicle counts on a single band: 0 = after
+ * each launch's last step (default), 1 = after every step (strict: the
+ * reference's per-step check, engine.cpp:219-224, at the cost of two more
+ * popcounts per 32 cells per step). */
+int bml_dev_set_census(bml_dev *dev, int every_step);
+
+/* TEST HOOK (fault injection, used by tests/ only): arms a fault for the NEXT
+ * bml_dev_step call — after `at_step` of its steps (0 <= at_step <= steps) the
+ * cell (row, col) (band-relative row) is toggled: Empty <-> LR, TB -> Empty.
+ * Up to 8 armed faults; single-band handles only. The call's launches are split
+ * at the fault, so the kernels that run are the normal ones. */
+int bml_dev_debug_fault(bml_dev *dev, int64_t at_step, int row, int col);
 
 /* Geometry of the last streaming-kernel launch: row strips, work items
  * (strips x warp columns) and CTAs. */

@@ -22,6 +22,8 @@
 //   ref_driver file    in=PATH n=N steps=T [backend=lanes] [threads=1]
 //                      [phase=h|v] [metrics=0|1] [dump_final=PATH]
 //   ref_driver bench   n=N rho=R seed=S steps=T backend=B [threads=0] [reps=5]
+//   ref_driver ladder  n=N rho=R seed=S plan=B:threads:steps:reps[,...]
+//                      [in=PATH expect_init=0xDIGEST]   (one init, several backends)
 //   ref_driver info
 // Lattice files are the n*n interior bytes, row-major (values 0/1/2).
 
@@ -231,24 +233,16 @@ int cmd_file(const Args& a) {
 // The reference's own bench method (tools/main.cpp:186-214): init once, then
 // per rep make_grid_pair (untimed) + steady_clock around run() without an
 // observer; mean and population stddev.
-int cmd_bench(const Args& a) {
-    const int n = std::stoi(need(a, "n"));
-    const double rho = std::stod(need(a, "rho"));
-    const std::uint64_t seed = std::stoull(get(a, "seed", "1"));
-    const long steps = std::stol(need(a, "steps"));
-    const int reps = std::stoi(get(a, "reps", "5"));
-    const bml::Backend backend = backend_arg(a);
-    const int threads = threads_arg(a, backend);
-
+std::string bench_backend(const bml::Grid& initial, double rho, std::uint64_t seed,
+                          bml::Backend backend, int threads, long steps, int reps) {
     bml::SimConfig cfg;
-    cfg.n = n;
+    cfg.n = initial.n();
     cfg.rho = rho;
     cfg.steps = steps;
     cfg.seed = seed;
     cfg.backend = backend;
     cfg.threads = threads;
     bml::validate(cfg);
-    const bml::Grid initial = bml::init_grid({n, rho, seed});
     std::vector<double> times;
     std::uint64_t digest = 0;
     for (int rep = 0; rep < reps; ++rep) {
@@ -271,13 +265,81 @@ int cmd_bench(const Args& a) {
         std::snprintf(buf, sizeof buf, "%s%.6f", i ? "," : "", times[i]);
         ts += buf;
     }
-    std::printf(
-        "{\"backend\":\"%s\",\"n\":%d,\"threads\":%d,\"reps\":%d,\"steps\":%ld,\"mean_s\":%.6f,"
-        "\"stddev_s\":%.6f,\"times\":[%s],\"final_digest\":%s,\"lane_width\":%d,"
-        "\"hardware_concurrency\":%u}\n",
-        std::string(bml::backend_name(backend)).c_str(), n, threads, reps, steps, mean,
-        std::sqrt(var), ts.c_str(), hex(digest).c_str(), bml::lane_width(),
-        std::thread::hardware_concurrency());
+    char head[512];
+    std::snprintf(head, sizeof head,
+                  "{\"backend\":\"%s\",\"n\":%d,\"threads\":%d,\"reps\":%d,\"steps\":%ld,\"mean_s\":%.6f,"
+                  "\"stddev_s\":%.6f,\"times\":[",
+                  std::string(bml::backend_name(backend)).c_str(), initial.n(), threads, reps, steps,
+                  mean, std::sqrt(var));
+    char tail[256];
+    std::snprintf(tail, sizeof tail,
+                  "],\"final_digest\":%s,\"lane_width\":%d,\"hardware_concurrency\":%u}",
+                  hex(digest).c_str(), bml::lane_width(), std::thread::hardware_concurrency());
+    return std::string(head) + ts + tail;
+}
+
+int cmd_bench(const Args& a) {
+    const int n = std::stoi(need(a, "n"));
+    const double rho = std::stod(need(a, "rho"));
+    const std::uint64_t seed = std::stoull(get(a, "seed", "1"));
+    const long steps = std::stol(need(a, "steps"));
+    const int reps = std::stoi(get(a, "reps", "5"));
+    const bml::Backend backend = backend_arg(a);
+    const int threads = threads_arg(a, backend);
+    const bml::Grid initial = bml::init_grid({n, rho, seed});
+    std::printf("%s\n", bench_backend(initial, rho, seed, backend, threads, steps, reps).c_str());
+    return 0;
+}
+
+// One input lattice, several backends: the reference bench method per backend
+// (bench_backend) after a SINGLE init — at n = 65536 the reference init_grid
+// alone takes ~8 min and ~43 GB (seeding.cpp:26-51), so the CPU arm cannot
+// afford one per backend. The lattice is the reference's own init_grid, or
+// (in=PATH) n*n interior bytes whose grid_digest must equal expect_init
+// (the reference init digest from the committed goldens).
+//   plan=backend:threads:steps:reps[,backend:threads:steps:reps...]
+int cmd_ladder(const Args& a) {
+    const int n = std::stoi(need(a, "n"));
+    const double rho = std::stod(need(a, "rho"));
+    const std::uint64_t seed = std::stoull(get(a, "seed", "1"));
+    const std::string in = get(a, "in", "");
+    const auto t0 = std::chrono::steady_clock::now();
+    const bml::Grid initial = in.empty() ? bml::init_grid({n, rho, seed}) : load_interior(in, n);
+    const double init_s =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const std::uint64_t init_digest = bml::grid_digest(initial);
+    const std::string expect = get(a, "expect_init", "");
+    if (!expect.empty() && std::stoull(expect, nullptr, 16) != init_digest)
+        throw std::runtime_error("ladder: input lattice digest " + hex(init_digest) +
+                                 " differs from expect_init " + expect);
+    std::string results;
+    std::string plan = need(a, "plan");
+    std::size_t pos = 0;
+    while (pos <= plan.size()) {
+        const std::size_t comma = std::min(plan.find(',', pos), plan.size());
+        const std::string item = plan.substr(pos, comma - pos);
+        pos = comma + 1;
+        if (item.empty()) continue;
+        std::vector<std::string> f;
+        std::size_t p = 0;
+        while (p <= item.size()) {
+            const std::size_t c = std::min(item.find(':', p), item.size());
+            f.push_back(item.substr(p, c - p));
+            p = c + 1;
+        }
+        if (f.size() != 4) throw std::invalid_argument("ladder: plan item must be backend:threads:steps:reps");
+        auto b = bml::backend_from_name(f[0]);
+        if (!b) throw std::invalid_argument("ladder: unknown backend " + f[0]);
+        Args ta;
+        ta["threads"] = f[1];
+        const int threads = threads_arg(ta, *b);
+        results += (results.empty() ? "" : ",") +
+                   bench_backend(initial, rho, seed, *b, threads, std::stol(f[2]), std::stoi(f[3]));
+    }
+    std::printf("{\"n\":%d,\"rho\":%.17g,\"seed\":%llu,\"init_source\":\"%s\",\"init_s\":%.6f,"
+                "\"init_digest\":%s,\"results\":[%s]}\n",
+                n, rho, static_cast<unsigned long long>(seed), in.empty() ? "init_grid" : "file",
+                init_s, hex(init_digest).c_str(), results.c_str());
     return 0;
 }
 
@@ -294,6 +356,7 @@ int main(int argc, char** argv) {
         if (cmd == "golden") return cmd_golden(a);
         if (cmd == "file") return cmd_file(a);
         if (cmd == "bench") return cmd_bench(a);
+        if (cmd == "ladder") return cmd_ladder(a);
         if (cmd == "info") {
             std::printf("{\"lane_width\":%d,\"hardware_concurrency\":%u}\n", bml::lane_width(),
                         std::thread::hardware_concurrency());

@@ -185,6 +185,13 @@ struct bml_dev {
     unsigned long long* down_flag = nullptr;  // neighbour below: its top flag
     std::vector<void*> ipc_opened;
     unsigned long long pubs = 0;
+    // census cadence (bml_dev_set_census) and armed test faults (bml_dev_debug_fault)
+    int census_every_step = 0;
+    struct Fault {
+        long long at;
+        int row, col;
+    };
+    std::vector<Fault> faults;
     // timing
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -597,9 +604,10 @@ bool cluster_launchable(ResidentKernel kern, int cluster, int threads) {
     return ok;
 }
 
-// (single band only: its metrics never need the per-step census, see bml_dev_step)
-int launch_resident(bml_dev* d, long long steps, bool count, bool census, bool* used) {
-    (void)census;
+// (single band only; with COUNT the kernels take the census after every step).
+// Metrics of step s of this launch go to d->metrics[q * metrics_stride + metrics_base + s].
+int launch_resident(bml_dev* d, long long steps, bool count, long long metrics_base, int metrics_stride,
+                    bool* used) {
     *used = false;
     for (int cluster : {16, 8, 4, 2, 1}) {
         int G = 0, rpw = 0, nw = 0, pack = 1;
@@ -629,8 +637,8 @@ int launch_resident(bml_dev* d, long long steps, bool count, bool census, bool* 
         ra.pitch = d->pitch;
         ra.ghost = G;
         ra.steps = steps;
-        ra.metrics = d->metrics;
-        ra.metrics_stride = static_cast<int>(steps);
+        ra.metrics = d->metrics ? d->metrics + metrics_base : nullptr;
+        ra.metrics_stride = metrics_stride;
         ra.error_flag = d->err + 1;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (d->timing) {
@@ -696,6 +704,7 @@ int bml_dev_destroy(bml_dev* d) {
     if (!d) return BML_OK;
     cudaSetDevice(d->device);
     if (d->stream) cudaStreamSynchronize(d->stream);
+    if (d->own_stream && d->own_stream != d->stream) cudaStreamSynchronize(d->own_stream);
     for (void* p : d->ipc_opened) cudaIpcCloseMemHandle(p);
     for (int p = 0; p < 2; ++p) cudaFree(d->buf[p]);
     cudaFree(d->staging);
@@ -716,7 +725,17 @@ int bml_dev_destroy(bml_dev* d) {
 
 int bml_dev_set_stream(bml_dev* d, void* stream) {
     if (int rc = check(d)) return rc;
-    d->stream = stream ? static_cast<cudaStream_t>(stream) : d->own_stream;
+    cudaStream_t next = stream ? static_cast<cudaStream_t>(stream) : d->own_stream;
+    if (next != d->stream) {
+        // order the work already queued on the old stream before the new one's
+        cudaEvent_t ev = take_event(d);
+        if (!ev) return fail(BML_ECUDA, "bml_dev_set_stream: cudaEventCreate failed");
+        cudaError_t e = cudaEventRecord(ev, d->stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(next, ev, 0);
+        d->ev_pool.push_back(ev);  // reusable: the wait captured the recorded work
+        if (e != cudaSuccess) return cuda_fail(e, "bml_dev_set_stream");
+    }
+    d->stream = next;
     return BML_OK;
 }
 
@@ -956,63 +975,127 @@ int bml_dev_phase(bml_dev* d, int phase, int64_t* moved) {
     return BML_OK;
 }
 
+int bml_dev_set_census(bml_dev* d, int every_step) {
+    if (int rc = check(d)) return rc;
+    if (every_step != 0 && every_step != 1) return fail(BML_EINVAL, "bml_dev_set_census: 0 or 1");
+    d->census_every_step = every_step;
+    return BML_OK;
+}
+
+int bml_dev_debug_fault(bml_dev* d, int64_t at_step, int row, int col) {
+    if (int rc = check(d)) return rc;
+    if (!d->single_band()) return fail(BML_EINVAL, "bml_dev_debug_fault: single-band handles only");
+    if (at_step < 0 || row < 0 || row >= d->rows || col < 0 || col >= d->n)
+        return fail(BML_EINVAL, "bml_dev_debug_fault: step/row/col out of range");
+    if (d->faults.size() >= 8) return fail(BML_EINVAL, "bml_dev_debug_fault: at most 8 armed faults");
+    d->faults.push_back({at_step, row, col});
+    return BML_OK;
+}
+
+namespace {
+
+// `seg` steps from step `from` of the current call: the resident kernel when the
+// lattice qualifies, else streaming launches of <= block_steps steps. `measured`
+// marks the steps whose census the kernels took.
+int run_segment(bml_dev* d, long long from, long long seg, bool count, bool every, int stride,
+                std::vector<char>& measured) {
+    bool resident_used = false;
+    if (int rc = launch_resident(d, seg, count, from, stride, &resident_used)) return rc;
+    if (resident_used) {
+        if (count) std::fill(measured.begin() + from, measured.begin() + from + seg, 1);
+        return BML_OK;
+    }
+    for (long long done = 0; done < seg;) {
+        const int k = largest_block_at_most(seg - done, d->block_steps);
+        if (int rc = launch_block(d, k, count, every, static_cast<int>(from + done), stride)) return rc;
+        if (count) {
+            if (every)
+                std::fill(measured.begin() + from + done, measured.begin() + from + done + k, 1);
+            else
+                measured[from + done + k - 1] = 1;  // COUNT 1: census after the launch's last step
+        }
+        done += k;
+    }
+    return BML_OK;
+}
+
+}  // namespace
+
 int bml_dev_step(bml_dev* d, int64_t steps, int64_t* lr_moved, int64_t* tb_moved,
                  int64_t* lr_count, int64_t* tb_count) {
     if (int rc = check(d)) return rc;
     if (steps < 0) return fail(BML_EINVAL, "bml_dev_step: steps must be >= 0");
-    if (steps == 0) return BML_OK;
+    if (!d->single_band() && !d->connected)
+        return fail(BML_EINVAL, "bml_dev_step: a partial row band must be connected (bml_dev_connect) "
+                                "before stepping");
+    std::vector<bml_dev::Fault> faults;
+    faults.swap(d->faults);  // armed for this call only
+    std::stable_sort(faults.begin(), faults.end(),
+                     [](const bml_dev::Fault& x, const bml_dev::Fault& y) { return x.at < y.at; });
+    if (steps == 0 && faults.empty()) return BML_OK;
     const bool count = lr_moved || tb_moved || lr_count || tb_count;
     if (count && steps > (1LL << 26))
         return fail(BML_EINVAL, "bml_dev_step: at most 2^26 steps per call with metrics");
-    // Vehicle counts (the reference's count_vehicles after every step). A whole
-    // torus conserves both species exactly (LR vehicles move within their row, TB
-    // vehicles within their column), so for a single band the per-step census is
-    // the count measured before the run, re-measured on the final lattice
-    // (BML_ECONSERVE on any difference): popcounting both planes after every step
-    // would triple the cost of the metrics path (the POPC pipe is the bottleneck).
-    // A row band's counts change as TB vehicles cross band edges, so bands count
-    // in the kernel.
+    // Vehicle census (the reference's count_vehicles after every step,
+    // engine.cpp:219-224), measured in the kernels: row bands and strict mode
+    // after every step (COUNT 2), a single band otherwise after each launch's
+    // last step (COUNT 1; the resident kernel always per step).
     const bool want_counts = lr_count || tb_count;
-    const bool census = want_counts && !d->single_band();
+    const bool banded = !d->single_band();
+    const bool every = want_counts && (banded || d->census_every_step);
     int64_t lr0 = 0, tb0 = 0;
-    if (want_counts && !census) {
+    if (want_counts && !banded) {
         if (int rc = bml_dev_counts(d, &lr0, &tb0)) return rc;
     }
     if (count) {
         if (int rc = ensure_metrics(d, steps)) return rc;
         BML_CUDA(cudaMemsetAsync(d->metrics, 0, 4 * steps * sizeof(unsigned long long), d->stream));
     }
+    std::vector<char> measured(count ? static_cast<size_t>(steps) : 0, 0);
     d->resident_cluster = 0;
-    bool resident_used = false;
-    if (int rc = launch_resident(d, steps, count, census, &resident_used)) return rc;
-    long long done = resident_used ? steps : 0;
-    while (done < steps) {
-        const int k = largest_block_at_most(steps - done, d->block_steps);
-        if (int rc = launch_block(d, k, count, census, static_cast<int>(done), static_cast<int>(steps)))
-            return rc;
-        done += k;
+    const int stride = static_cast<int>(steps);
+    long long done = 0;
+    size_t fi = 0;
+    for (;;) {
+        for (; fi < faults.size() && faults[fi].at <= done; ++fi) {  // injected faults due now
+            if (faults[fi].at > steps) continue;
+            debug_toggle_kernel<<<1, 32, 0, d->stream>>>(d->row0(d->cur), d->pitch, faults[fi].row,
+                                                         faults[fi].col);
+            BML_CUDA(cudaGetLastError());
+            if (int rc = fill_images(d, d->cur)) return rc;
+        }
+        if (done >= steps) break;
+        long long seg_end = steps;
+        if (fi < faults.size() && faults[fi].at < steps) seg_end = faults[fi].at;
+        if (int rc = run_segment(d, done, seg_end - done, count, every, stride, measured)) return rc;
+        done = seg_end;
     }
-    if (count) {
-        std::vector<unsigned long long> h(static_cast<size_t>(4 * steps));
-        BML_CUDA(cudaMemcpyAsync(h.data(), d->metrics, h.size() * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, d->stream));
-        BML_CUDA(cudaStreamSynchronize(d->stream));
-        if (want_counts && !census) {
-            int64_t lr1 = 0, tb1 = 0;
-            if (int rc = bml_dev_counts(d, &lr1, &tb1)) return rc;
-            if (lr1 != lr0 || tb1 != tb0)
-                return fail(BML_ECONSERVE, "conservation violated within steps 1.." +
-                                               std::to_string(steps) + ": lr " + std::to_string(lr1) +
-                                               "/" + std::to_string(lr0) + ", tb " +
-                                               std::to_string(tb1) + "/" + std::to_string(tb0));
+    if (!count) return BML_OK;
+    std::vector<unsigned long long> h(static_cast<size_t>(4 * steps));
+    BML_CUDA(cudaMemcpyAsync(h.data(), d->metrics, h.size() * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, d->stream));
+    BML_CUDA(cudaStreamSynchronize(d->stream));
+    if (int rc = check_errors(d)) return rc;
+    int64_t lc = lr0, tc = tb0;
+    long long violated = -1;
+    for (int64_t s = 0; s < steps; ++s) {
+        if (measured[s]) {
+            lc = static_cast<int64_t>(h[2 * steps + s]);
+            tc = static_cast<int64_t>(h[3 * steps + s]);
+            if (want_counts && !banded && violated < 0 && (lc != lr0 || tc != tb0)) violated = s;
         }
-        for (int64_t s = 0; s < steps; ++s) {
-            if (lr_moved) lr_moved[s] = static_cast<int64_t>(h[s]);
-            if (tb_moved) tb_moved[s] = static_cast<int64_t>(h[steps + s]);
-            if (lr_count) lr_count[s] = census ? static_cast<int64_t>(h[2 * steps + s]) : lr0;
-            if (tb_count) tb_count[s] = census ? static_cast<int64_t>(h[3 * steps + s]) : tb0;
-        }
-        return check_errors(d);
+        if (lr_moved) lr_moved[s] = static_cast<int64_t>(h[s]);
+        if (tb_moved) tb_moved[s] = static_cast<int64_t>(h[steps + s]);
+        if (lr_count) lr_count[s] = lc;
+        if (tb_count) tb_count[s] = tc;
+    }
+    if (violated >= 0) {
+        const int64_t vl = static_cast<int64_t>(h[2 * steps + violated]);
+        const int64_t vt = static_cast<int64_t>(h[3 * steps + violated]);
+        return fail(BML_ECONSERVE, "conservation violated at step " + std::to_string(violated + 1) + " of " +
+                                       std::to_string(steps) + ": lr " + std::to_string(vl) + "/" +
+                                       std::to_string(lr0) + ", tb " + std::to_string(vt) + "/" +
+                                       std::to_string(tb0));
     }
     return BML_OK;
 }
@@ -1134,6 +1217,8 @@ int bml_dev_connect_local(bml_dev* d, bml_dev* up, bml_dev* down) {
 
 int bml_dev_exchange_halos(bml_dev* d) {
     if (int rc = check(d)) return rc;
+    if (!d->connected && !d->single_band())
+        return fail(BML_EINVAL, "bml_dev_exchange_halos: a partial row band must be connected first");
     if (!d->connected) return fill_images(d, d->cur);
     push_halo_kernel<<<1, 1024, 0, d->stream>>>(d->row0(d->cur), d->W, d->pitch, d->rows,
                                                 d->up_halo[d->cur], d->down_halo[d->cur],

@@ -202,9 +202,10 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(const ResidentArgs a)
                 const uint32_t nt = (above & ~Op[i]) | (T[i] & below);
                 if (COUNT) {
                     const int e = erow(i);
-                    if (e >= G && e < G + B) {
+                    if (e >= G && e < G + B) {  // owned rows: moved, and the census after the step
                         tb_moved += __popc(T[i] & ~below & valid);
-
+                        lr_cnt += __popc(L[i] & valid);
+                        tb_cnt += __popc(nt & valid);
                     }
                 }
                 T[i] = nt;
@@ -372,9 +373,10 @@ __global__ void __launch_bounds__(1024, 1) resident_p2p_kernel(const ResidentArg
             const uint32_t above = i > 0 ? T[i - 1] : t_up;
             const uint32_t below = i < RPW - 1 ? Op[i + 1] : o_dn;
             const uint32_t nt = (above & ~Op[i]) | (T[i] & below);
-            if (COUNT) {
+            if (COUNT) {  // moved, and the census after the step
                 tb_moved += __popc(T[i] & ~below & valid);
-
+                lr_cnt += __popc(L[i] & valid);
+                tb_cnt += __popc(nt & valid);
             }
             T[i] = nt;
         }

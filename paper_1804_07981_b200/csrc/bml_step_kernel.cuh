@@ -157,7 +157,11 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
             if (static_cast<unsigned>(rho - c.r_lo) < span) q.cm[s] += __popc(L & ~nextO & c.valid);
             if (static_cast<unsigned>(rho - 1 - c.r_lo) < span) {
                 q.cm[s] += static_cast<uint32_t>(__popc(tB & ~Op & c.valid)) << 16;
-                if (COUNT == 2)  // per-step vehicle census (row bands: TB vehicles cross bands)
+                // vehicle census of the emitted row: after every step (COUNT 2: row
+                // bands, whose counts change as TB vehicles cross band edges, and the
+                // strict single-band mode), or only after the launch's last step
+                // (COUNT 1: the census at launch boundaries, one row in K stages)
+                if (COUNT == 2 || s == K - 1)
                     q.cc[s] += __popc(newL & c.valid) +
                                (static_cast<uint32_t>(__popc(newT & c.valid)) << 16);
             }
@@ -176,8 +180,9 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
 // register file (<= 168 registers); the 256-thread one (at most two warps per
 // SMSP, the latency-bound regime of mid-size lattices) may use up to 255
 // registers, and ptxas schedules it with fewer moves (+4% at N=8192).
-// COUNT: 0 no metrics; 1 moved counts per step; 2 also the per-step vehicle
-// census (row bands only, see bml_dev_step)
+// COUNT: 0 no metrics; 1 moved counts per step + the vehicle census after the
+// launch's last step; 2 moved counts + the census after every step (row bands,
+// strict single-band mode; see bml_dev_step)
 template <int K, int MODE, int COUNT, int MAXT = kMaxWarpsPerCta * 32>
 __global__ void __launch_bounds__(MAXT, 1)
 step_block_kernel(const StepArgs a) {
@@ -335,8 +340,9 @@ step_block_kernel(const StepArgs a) {
             for (int s = 0; s < K; ++s) {
                 const unsigned v0 = __reduce_add_sync(kFull, q.cm[s] & 0xffffu);
                 const unsigned v1 = __reduce_add_sync(kFull, q.cm[s] >> 16);
-                const unsigned v2 = COUNT == 2 ? __reduce_add_sync(kFull, q.cc[s] & 0xffffu) : 0u;
-                const unsigned v3 = COUNT == 2 ? __reduce_add_sync(kFull, q.cc[s] >> 16) : 0u;
+                const bool census = COUNT == 2 || s == K - 1;
+                const unsigned v2 = census ? __reduce_add_sync(kFull, q.cc[s] & 0xffffu) : 0u;
+                const unsigned v3 = census ? __reduce_add_sync(kFull, q.cc[s] >> 16) : 0u;
                 if (lane == 0) {
                     unsigned long long* m = a.metrics + a.step_base + s;
                     if (v0) atomicAdd(m, static_cast<unsigned long long>(v0));

@@ -202,4 +202,17 @@ __global__ void counts_kernel(const uint2* __restrict__ buf, int W, int pitch, i
 }
 
 
+// TEST HOOK (bml_dev_debug_fault): toggle one cell, Empty <-> LR, TB -> Empty.
+__global__ void debug_toggle_kernel(uint2* row0, int pitch, int row, int col) {
+    if (threadIdx.x != 0) return;
+    uint2* w = row0 + static_cast<long long>(row) * pitch + (col >> 5);
+    const uint32_t bit = 1u << (col & 31);
+    uint2 v = *w;
+    if (v.y & bit)
+        v.y &= ~bit;
+    else
+        v.x ^= bit;
+    *w = v;
+}
+
 }  // namespace bml_k

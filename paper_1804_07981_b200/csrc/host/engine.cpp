@@ -205,14 +205,25 @@ void DeviceLattice::step(long steps) {
     }
 }
 
-std::vector<StepMetrics> DeviceLattice::step_with_metrics(long steps, long first_step) {
+void DeviceLattice::set_census(bool every_step) {
+    for (bml_dev* h : bands_) ok(bml_dev_set_census(h, every_step ? 1 : 0), "bml_dev_set_census");
+}
+
+void DeviceLattice::debug_fault(long at_step, int row, int col) {
+    if (bands_.size() != 1) throw std::invalid_argument("debug_fault: single-band lattices only");
+    ok(bml_dev_debug_fault(bands_[0], at_step, row, col), "bml_dev_debug_fault");
+}
+
+std::vector<StepMetrics> DeviceLattice::step_with_metrics(long steps, long first_step,
+                                                          bool throw_on_violation) {
     if (steps < 0) throw std::invalid_argument("step: steps must be >= 0");
     std::vector<StepMetrics> out(static_cast<std::size_t>(steps));
     if (steps == 0) return out;
     std::vector<std::int64_t> lm(steps, 0), tm(steps, 0), lc(steps, 0), tc(steps, 0);
     if (bands_.size() == 1) {
+        // BML_ECONSERVE still fills the arrays (through the violating step)
         const int rc = bml_dev_step(bands_[0], steps, lm.data(), tm.data(), lc.data(), tc.data());
-        if (rc != BML_OK && rc != BML_ECONSERVE) raise(rc, "bml_dev_step");
+        if (rc != BML_OK && (rc != BML_ECONSERVE || throw_on_violation)) raise(rc, "bml_dev_step");
     } else {
         std::vector<std::int64_t> a(16), b(16), c(16), d(16);
         for (long done = 0; done < steps;) {
@@ -348,6 +359,7 @@ Grid run(const SimConfig& cfg, GridPair& pair, const StepObserver& observer) {
     if (pair.cur.n() != cfg.n) throw std::invalid_argument("run: grid size does not match config");
     if (cfg.steps > 0) check_pair("run", pair, cfg.backend, cfg.threads);
     DeviceLattice& dev = lattice_for(cfg.n, cfg.devices);
+    dev.set_census(cfg.strict_census);
     dev.upload(pair.cur);
     if (!observer) {
         dev.step(cfg.steps);
@@ -366,7 +378,7 @@ Grid run(const SimConfig& cfg, GridPair& pair, const StepObserver& observer) {
     if (cfg.observer_reads_grid) {
         // reference contract: pair.cur holds the post-step grid at every call
         for (long s = 1; s <= cfg.steps; ++s) {
-            const std::vector<StepMetrics> m = dev.step_with_metrics(1, s);
+            const std::vector<StepMetrics> m = dev.step_with_metrics(1, s, false);
             dev.download(pair.cur);
             deliver(m[0]);
         }
@@ -374,7 +386,7 @@ Grid run(const SimConfig& cfg, GridPair& pair, const StepObserver& observer) {
         constexpr long kChunk = 1L << 16;
         for (long s = 1; s <= cfg.steps; s += kChunk) {
             const long k = std::min(kChunk, cfg.steps - s + 1);
-            for (const StepMetrics& m : dev.step_with_metrics(k, s)) deliver(m);
+            for (const StepMetrics& m : dev.step_with_metrics(k, s, false)) deliver(m);
         }
         dev.download(pair.cur);
     }

@@ -62,6 +62,8 @@ struct SimConfig {
     // --- extensions (defaults keep reference call sites valid) ---
     int devices = 1;                  // row bands (GPUs); placed round-robin on visible GPUs
     bool observer_reads_grid = true;  // download pair.cur before every observer call
+    bool strict_census = false;       // single band: vehicle census after every step, not
+                                      // only at launch boundaries (bml_dev_set_census)
 };
 
 void validate(const SimConfig& cfg);
@@ -103,8 +105,18 @@ public:
 
     void step(long steps);
     // Per-step metrics for `steps` steps; step indices start at first_step.
-    // Throws std::logic_error on a conservation violation (engine.cpp:219-224).
-    std::vector<StepMetrics> step_with_metrics(long steps, long first_step = 1);
+    // Throws std::logic_error on a conservation violation (engine.cpp:219-224)
+    // unless throw_on_violation is false: then the metrics come back with the
+    // measured (violating) counts and the caller decides (run() throws at the
+    // first step whose counts differ, delivering the steps before it).
+    std::vector<StepMetrics> step_with_metrics(long steps, long first_step = 1,
+                                               bool throw_on_violation = true);
+    // Vehicle-census cadence on a single band: after every step (true) or after
+    // each launch's last step (false, default). See bml_dev_set_census.
+    void set_census(bool every_step);
+    // TEST HOOK: toggle cell (row, col) after `at_step` steps of the next
+    // step()/step_with_metrics() call (bml_dev_debug_fault). Single band only.
+    void debug_fault(long at_step, int row, int col);
     std::int64_t phase(Phase p);  // returns moved_in_phase
     VehicleCounts counts() const;
     // grid_digest (digest.hpp) of the device lattice, computed on the GPU(s).

@@ -22,7 +22,18 @@ std::optional<GridMismatch> first_mismatch(const std::vector<NamedGrid>& grids) 
 
 namespace {
 
+// Row bands for the banded path: the largest g <= 4 whose ceil(n/g) split
+// (engine.cpp:131-137) leaves every band >= 16 rows (the ghost depth), else 1.
+int verify_bands(int n) {
+    for (int g = 4; g >= 2; --g) {
+        const int band = (n + g - 1) / g;
+        if (n - (g - 1) * band >= 16) return g;
+    }
+    return 1;
+}
+
 bool conserved_run(DeviceLattice& lat, long steps, const VehicleCounts& initial) {
+    lat.set_census(true);  // the reference's per-step check, exactly (verify.cpp:27-30)
     try {
         const auto metrics = lat.step_with_metrics(steps);
         for (const StepMetrics& m : metrics)
@@ -72,7 +83,7 @@ VerifyReport verify_backends(const SimConfig& cfg) {
         record("b200-phases", lat);
     }
     {  // row bands with in-kernel ghost-row exchange (block depth 1 when too small)
-        const int bands = std::clamp(cfg.n / 16, 1, 4);
+        const int bands = verify_bands(cfg.n);
         DeviceLattice lat(cfg.n, bands);
         if (bands == 1) lat.configure(1, 0);
         lat.upload(initial);

@@ -40,13 +40,14 @@ bml::Grid step_many(const bml::Grid& grid, long steps, bml::Backend backend, int
 
 std::pair<bml::Grid, std::vector<bml::StepMetrics>> simulate(const bml::Grid& grid, long steps,
                                                              bml::Backend backend, int threads,
-                                                             int devices) {
+                                                             int devices, bool strict_census) {
     bml::SimConfig cfg;
     cfg.n = grid.n();
     cfg.steps = steps;
     cfg.backend = backend;
     cfg.threads = threads;
     cfg.devices = devices;
+    cfg.strict_census = strict_census;
     cfg.observer_reads_grid = false;  // the collector below never reads the grid
     bml::GridPair pair = bml::make_grid_pair(backend, grid);
     std::vector<bml::StepMetrics> metrics;
@@ -213,7 +214,10 @@ PYBIND11_MODULE(_bml, m) {
 
     m.def("simulate", &simulate, py::arg("grid"), py::arg("steps"),
           py::arg("backend") = bml::Backend::B200, py::arg("threads") = 1, py::arg("devices") = 1,
-          "Advance and record per-step metrics; returns (grid, [StepMetrics]).");
+          py::arg("strict_census") = false,
+          "Advance and record per-step metrics; returns (grid, [StepMetrics]). strict_census: "
+          "vehicle census after every step (the reference's exact per-step check) rather than "
+          "at launch boundaries.");
 
     m.def("count_vehicles",
           [](const bml::Grid& g) {
@@ -250,7 +254,11 @@ PYBIND11_MODULE(_bml, m) {
         .def("step", &bml::DeviceLattice::step, py::arg("steps"),
              py::call_guard<py::gil_scoped_release>())
         .def("step_with_metrics", &bml::DeviceLattice::step_with_metrics, py::arg("steps"),
-             py::arg("first_step") = 1, py::call_guard<py::gil_scoped_release>())
+             py::arg("first_step") = 1, py::arg("throw_on_violation") = true,
+             py::call_guard<py::gil_scoped_release>())
+        .def("set_census", &bml::DeviceLattice::set_census, py::arg("every_step"))
+        .def("debug_fault", &bml::DeviceLattice::debug_fault, py::arg("at_step"), py::arg("row"),
+             py::arg("col"), "TEST HOOK: toggle a cell after at_step steps of the next step call.")
         .def("phase", &bml::DeviceLattice::phase, py::arg("phase"),
              py::call_guard<py::gil_scoped_release>())
         .def("counts",

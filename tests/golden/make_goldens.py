@@ -11,6 +11,10 @@ GPU box (which has no /root/reference) can check the CUDA path against it.
     python tests/golden/make_goldens.py c4short    # N=65536, 1000 steps (~45 min, 43 GB RAM)
     python tests/golden/make_goldens.py c4         # N=65536, 10000 steps (~6 h, 43 GB RAM)
     python tests/golden/make_goldens.py regimes    # N=256, rho .25/.38, seeds 1-10, 4096 steps (~1 min)
+    python tests/golden/make_goldens.py c4chain WORKDIR
+                                                   # N=65536, 10000 steps as ten resumable 1000-step
+                                                   # legs (golden leg, then `file` legs on the dumped
+                                                   # lattice); same digest as `c4`, restartable
 
 Every record holds the reference's init digest, final digest after `steps`
 full steps, the vehicle counts and (where metrics=1) the observer-path sums
@@ -87,8 +91,58 @@ def run_regimes():
     print("wrote", out)
 
 
+def run_chain(n, rho, seed, steps, leg, work):
+    """One long golden as resumable legs of `leg` steps.
+
+    Leg 0 is `ref_driver golden` (the reference's own init_grid, then `leg` steps); each
+    later leg is `ref_driver file` on the previous leg's dumped interior. The reference
+    stepping is a pure function of the lattice (engine.cpp:206-208), so the chained
+    final digest equals an unbroken run's. Every leg's record is kept in the output as
+    an intermediate checkpoint digest.
+    """
+    os.makedirs(work, exist_ok=True)
+    log = os.path.join(work, "legs.jsonl")
+    legs = []
+    if os.path.exists(log):
+        legs = [json.loads(l) for l in open(log) if l.strip()]
+    done = len(legs) * leg
+    while done < steps:
+        out_bin = os.path.join(work, f"s{done + leg}.bin")
+        if done == 0:
+            args = [DRIVER, "golden", f"n={n}", f"rho={rho}", f"seed={seed}", f"steps={leg}",
+                    "metrics=0", "backend=lanes", f"dump_final={out_bin}"]
+        else:
+            args = [DRIVER, "file", f"in={os.path.join(work, f's{done}.bin')}", f"n={n}",
+                    f"steps={leg}", "metrics=0", "backend=lanes", f"dump_final={out_bin}"]
+        print("running", " ".join(args), flush=True)
+        rec = json.loads(subprocess.run(args, check=True, capture_output=True, text=True).stdout)
+        rec["at_step"] = done + leg
+        with open(log, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+        legs.append(rec)
+        if done > 0:
+            os.remove(os.path.join(work, f"s{done}.bin"))
+        done += leg
+        print("leg", done, rec["final_digest"], flush=True)
+    first, last = legs[0], legs[-1]
+    out = {"n": n, "rho": rho, "seed": seed, "steps": steps, "backend": "lanes", "threads": 1,
+           "k": first["k"], "init_digest": first["init_digest"], "final_digest": last["final_digest"],
+           "lr_count": last["lr_count"], "tb_count": last["tb_count"], "init_s": first["init_s"],
+           "run_s": sum(r["run_s"] for r in legs),
+           "checkpoints": [{"step": r["at_step"], "digest": r["final_digest"]} for r in legs],
+           "generator": ("oracle/_ref/ref_driver (unmodified reference sources, lanes backend), "
+                         f"{len(legs)} chained legs of {leg} steps (make_goldens.py c4chain)")}
+    path = os.path.join(HERE, name_of(dict(n=n, rho=rho, seed=seed, steps=steps)))
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    print("wrote", path, out["final_digest"], flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "small"
+    if which == "c4chain":
+        run_chain(65536, 0.35, 1, 10000, 1000, sys.argv[2])
+        sys.exit(0)
     if which == "regimes":
         run_regimes()
         sys.exit(0)

@@ -6,7 +6,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,rho,steps,seed", [(33, 0.5, 20, 7), (64, 0.38, 45, 1),
+@pytest.mark.parametrize("n,rho,steps,seed", [(33, 0.5, 20, 7), (49, 0.35, 21, 2), (64, 0.38, 45, 1),
+                                              (65, 0.3, 19, 4), (66, 0.4, 17, 5), (69, 0.35, 23, 6),
                                               (100, 0.3, 33, 3), (1024, 0.38, 50, 1)])
 def test_four_identical_digests(gpu, oracle, n, rho, steps, seed):
     report = gpu.verify_backends(n, rho, steps, seed, 2)
