@@ -169,6 +169,12 @@ int bml_dev_set_census(bml_dev *dev, int every_step);
  * at the fault, so the kernels that run are the normal ones. */
 int bml_dev_debug_fault(bml_dev *dev, int64_t at_step, int row, int col);
 
+/* Streaming-kernel variant: 0 = automatic (default), 1 = narrow (32 cells per
+ * lane, K <= 16 steps per launch), 2 / 3 = wide (64 cells per lane, TMA
+ * bulk-copied rows, K = 14 / 12 steps per launch; n % 64 == 0 and n >= 2048
+ * only, else narrow). Row bands: set on every band before connecting. */
+int bml_dev_set_variant(bml_dev *dev, int variant);
+
 /* Geometry of the last streaming-kernel launch: row strips, work items
  * (strips x warp columns) and CTAs. */
 int bml_dev_last_launch(bml_dev *dev, int *nstrips, int *items, int *grid);

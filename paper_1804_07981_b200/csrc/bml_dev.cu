@@ -54,6 +54,7 @@
 #include "bml_resident_kernel.cuh"
 #include "bml_step_kernel.cuh"
 #include "bml_support_kernels.cuh"
+#include "bml_wide_kernel.cuh"
 
 using namespace bml_k;  // the kernels and their helpers (bml_kernels_common.cuh and friends)
 
@@ -121,6 +122,16 @@ int warps_per_smsp(StepKernel kern) {
     return u;
 }
 
+// wide-lane kernel (64 cells per lane, TMA bulk row ring). Its pipeline state
+// is twice the narrow kernel's per stage, so K = 16 spills: K = 14 (bare loop,
+// 252 registers) and K = 12 (all metric modes). The run's tail blocks (fewer
+// steps left than K) use the narrow kernel.
+StepKernel pick_wide(int k, int count, bool tma = true) {
+    if (k == 14 && count == 0) return tma ? step_wide_kernel<14, 0, true> : step_wide_kernel<14, 0, false>;
+    if (k == 12) return count == 2 ? step_wide_kernel<12, 2> : count ? step_wide_kernel<12, 1> : step_wide_kernel<12, 0>;
+    return nullptr;
+}
+
 // count: 0 no metrics, 1 moved counts, 2 moved counts + vehicle census
 StepKernel pick(int k, int mode, int count) {
     if (mode == kFullRow)
@@ -158,6 +169,7 @@ struct bml_dev {
     int device = 0;
     uint32_t last_mask = kFull;
     int mode = kGeneric;
+    int variant = 0;  // streaming kernel: 0 auto, 1 narrow (32 cells/lane), 2 / 3 wide (64 cells/lane), K 14 / 12
     int block_steps = 16;
     int strip_rows = 0;      // 0 = auto (choose_nstrips); < 0: exactly -strip_rows strips
     int resident = 1;        // 1: use the cluster-resident kernel when the lattice qualifies
@@ -184,7 +196,7 @@ struct bml_dev {
     unsigned long long* up_flag = nullptr;    // neighbour above: its bottom flag
     unsigned long long* down_flag = nullptr;  // neighbour below: its top flag
     std::vector<void*> ipc_opened;
-    unsigned long long pubs = 0;
+    unsigned long long pub_sum = 0;  // flag value the neighbours have reached before the next launch
     // census cadence (bml_dev_set_census) and armed test faults (bml_dev_debug_fault)
     int census_every_step = 0;
     struct Fault {
@@ -201,7 +213,14 @@ struct bml_dev {
 
     uint2* row0(int parity) const { return buf[parity] + static_cast<long long>(kHalo) * pitch; }
     bool single_band() const { return rows == n && row_begin == 0; }
-    int ncols() const {
+    // the wide-lane kernel: aligned rows of >= 64 words, an even word count
+    bool wide_ok() const { return mode == kAligned && W >= 64 && W % 2 == 0; }
+    bool use_wide() const { return variant != 1 && wide_ok() && (variant >= 2 || wide_auto()); }
+    // steps per wide launch for a metrics mode (0 = bare loop)
+    int wide_depth(int metrics) const { return metrics == 0 && variant != 3 ? 14 : 12; }
+    bool wide_auto() const { return false; }
+    int ncols() const { return use_wide() ? (W + kWideOut - 1) / kWideOut : narrow_ncols(); }
+    int narrow_ncols() const {
         if (mode == kFullRow) return 1;
         const int out = mode == kSeam ? kSeamOutWords : kOutWords;
         return (W + out - 1) / out;
@@ -361,11 +380,11 @@ long long smsp_round_cost(long long w) {
     return 780 + (u - 3) * 260;
 }
 
-int choose_nstrips(const bml_dev* d, int k, int warps_per_sm) {
+int choose_nstrips(const bml_dev* d, int k, int warps_per_sm, int ncols) {
     const int min_rows = d->connected ? kHalo : 1;
     if (d->strip_rows > 0) return std::max(1, d->rows / std::max(d->strip_rows, min_rows));
     if (d->strip_rows < 0) return std::max(1, std::min(-d->strip_rows, d->rows / min_rows));
-    const long long cols = d->ncols();
+    const long long cols = ncols;
     const int max_strips = std::max(1, d->rows / min_rows);
     long long best_cost = -1;
     int best = 1;
@@ -385,20 +404,22 @@ int choose_nstrips(const bml_dev* d, int k, int warps_per_sm) {
 
 int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int metrics_stride) {
     const int metrics = count ? (census ? 2 : 1) : 0;
-    StepKernel kern = pick(k, d->mode, metrics);
+    const bool wide = d->use_wide() && pick_wide(k, metrics);
+    StepKernel kern = wide ? pick_wide(k, metrics, d->variant != 4) : pick(k, d->mode, metrics);
     if (!kern) return fail(BML_EINVAL, "unsupported block depth " + std::to_string(k));
     const int u_max = warps_per_smsp(kern);  // 3 at <= 168 registers/thread
     // every strip has >= min(strip_rows, 16) rows, so for connected bands the
     // ghost-row sources of a band never straddle strips
     // the model scans every strip count: memoised per (k, strip setting)
     if (d->ns_cache_k[k] <= 0 || d->ns_cache_setting[k] != d->strip_rows) {
-        d->ns_cache_k[k] = choose_nstrips(d, k, 4 * u_max);
+        d->ns_cache_k[k] = choose_nstrips(d, k, 4 * (wide ? std::min(2, u_max) : u_max),
+                                          wide ? d->ncols() : d->narrow_ncols());
         d->ns_cache_setting[k] = d->strip_rows;
     }
     int nstrips = d->ns_cache_k[k];
     // metrics kernels pack two per-lane counters into 16-bit halves: a strip
     // may hold at most 2047 rows (32 cells per lane and row)
-    if (count) nstrips = std::max(nstrips, (d->rows + 2046) / 2047);
+    if (count) nstrips = std::max(nstrips, wide ? (d->rows + 1022) / 1023 : (d->rows + 2046) / 2047);
     const int strip = d->rows / nstrips;
     StepArgs a{};
     a.src = d->row0(d->cur);
@@ -409,7 +430,7 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
     a.rows = d->rows;
     a.strip_rows = strip;
     a.nstrips = nstrips;
-    a.ncols = d->ncols();
+    a.ncols = wide ? d->ncols() : d->narrow_ncols();
     a.items = nstrips * a.ncols;
     a.last_mask = d->last_mask;
     a.single_band = d->connected ? 0 : 1;
@@ -420,7 +441,9 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
     a.down_flag = d->down_flag;
     a.top_flag = d->flags;
     a.bot_flag = d->flags + 1;
-    a.expect = d->pubs * static_cast<unsigned long long>(a.ncols);
+    // every edge warp of a launch adds 1 to the neighbour's flag; all bands run the
+    // same launch sequence, so the expected value is the running sum of ncols
+    a.expect = d->pub_sum;
     a.metrics = d->metrics;
     a.metrics_stride = metrics_stride;
     a.step_base = step_base;
@@ -439,10 +462,10 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
     }
 
     // one CTA per SM with 4u warps, u = the warps per SMSP the items need
-    const int u = std::min(u_max, std::max(1, (a.items + 4 * d->sms - 1) / (4 * d->sms)));
+    const int u = std::min(wide ? 2 : u_max, std::max(1, (a.items + 4 * d->sms - 1) / (4 * d->sms)));
     const int grid = std::max(1, std::min(d->sms, a.items));
     const int threads = 4 * u * 32;
-    if (u <= 2) {
+    if (u <= 2 && !wide) {
         if (StepKernel narrow = pick_narrow(k, d->mode, metrics)) kern = narrow;
     }
     d->last_nstrips = nstrips;
@@ -481,7 +504,7 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
     }
     ++d->launches;
     d->cur ^= 1;
-    if (d->connected) ++d->pubs;
+    if (d->connected) d->pub_sum += static_cast<unsigned long long>(a.ncols);
     return BML_OK;
 }
 
@@ -771,6 +794,16 @@ int bml_dev_set_resident(bml_dev* d, int mode) {
     return BML_OK;
 }
 
+int bml_dev_set_variant(bml_dev* d, int variant) {
+    if (int rc = check(d)) return rc;
+    if (variant < 0 || variant > 4) return fail(BML_EINVAL, "bml_dev_set_variant: 0 (auto), 1, 2, 3 or 4");
+    if (d->connected)
+        return fail(BML_EINVAL, "bml_dev_set_variant: set before bml_dev_connect (all bands alike)");
+    d->variant = variant;
+    std::fill(std::begin(d->ns_cache_k), std::end(d->ns_cache_k), 0);
+    return BML_OK;
+}
+
 int bml_dev_path(bml_dev* d, int* resident_cluster) {
     if (!d) return fail(BML_EINVAL, "null bml_dev handle");
     if (resident_cluster) *resident_cluster = d->resident_cluster;
@@ -1005,8 +1038,10 @@ int run_segment(bml_dev* d, long long from, long long seg, bool count, bool ever
         if (count) std::fill(measured.begin() + from, measured.begin() + from + seg, 1);
         return BML_OK;
     }
+    const int metrics = count ? (every ? 2 : 1) : 0;
+    const int wk = d->use_wide() && d->block_steps == 16 ? d->wide_depth(metrics) : 0;
     for (long long done = 0; done < seg;) {
-        const int k = largest_block_at_most(seg - done, d->block_steps);
+        const int k = (wk && seg - done >= wk) ? wk : largest_block_at_most(seg - done, d->block_steps);
         if (int rc = launch_block(d, k, count, every, static_cast<int>(from + done), stride)) return rc;
         if (count) {
             if (every)
@@ -1224,7 +1259,7 @@ int bml_dev_exchange_halos(bml_dev* d) {
                                                 d->up_halo[d->cur], d->down_halo[d->cur],
                                                 d->up_flag, d->down_flag, d->ncols());
     BML_CUDA(cudaGetLastError());
-    ++d->pubs;
+    d->pub_sum += static_cast<unsigned long long>(d->ncols());
     return BML_OK;
 }
 
