@@ -177,6 +177,8 @@ def load_abi():
     lib.bml_dev_destroy.argtypes = [vp]
     lib.bml_dev_upload.argtypes = [vp, vp, ctypes.c_size_t]
     lib.bml_dev_download.argtypes = [vp, vp, ctypes.c_size_t]
+    lib.bml_dev_upload_async.argtypes = [vp, vp, ctypes.c_size_t]
+    lib.bml_dev_download_async.argtypes = [vp, vp, ctypes.c_size_t]
     lib.bml_dev_step.argtypes = [vp, ctypes.c_int64, vp, vp, vp, vp]
     lib.bml_dev_set_stream.argtypes = [vp, vp]
     lib.bml_dev_sync.argtypes = [vp]
@@ -430,10 +432,12 @@ def run_b200(args, wl):
     golden = find_golden(n, rho, seed, steps)
     parity = parity_check(bml, lat, n, rho, seed, golden)
 
-    # e2e through the C-ABI with pinned host buffers
+    # e2e through the C-ABI with pinned host buffers: pipelined over two handles
+    # (the contract's e2e), and one synchronous call sequence at a time
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(abi, torch, bml, grid, n, steps, args, golden)
+        e2e = run_e2e_pipelined(abi, torch, bml, grid, n, steps, args, golden)
+        e2e["sync"] = run_e2e(abi, torch, bml, grid, n, steps, args, golden)
 
     cpu = None
     if not args.no_cpu and rank == 0:
@@ -514,6 +518,61 @@ def cpu_baseline_b200_arm(grid, n, rho, seed, steps, golden):
     return cpu_baseline_record(res, steps, 3)
 
 
+def check_result(bml, n, data, golden, steps):
+    """The downloaded lattice's host grid_digest against the reference golden."""
+    if golden is None or golden["steps"] != steps:
+        return None
+    d = bml.Grid.from_bytes(n, data).digest()
+    check = {"golden": golden["file"], "digest": f"0x{d:016x}", "match": f"0x{d:016x}" == golden["final_digest"]}
+    assert check["match"], f"e2e result differs from the reference golden: {check}"
+    return check
+
+
+def run_e2e_pipelined(abi, torch, bml, grid, n, steps, args, golden):
+    """Bench steps as independent jobs through the asynchronous C-ABI: job i uploads
+    its input from pinned host memory, runs `steps` steps and downloads its result,
+    all on handle i % 2's stream, so one job's PCIe transfers (and pack/unpack)
+    overlap the other job's stepping. Every job's H2D and D2H are inside the timed
+    region (host clock around all jobs, both streams synchronised at the end)."""
+    vp = ctypes.c_void_p
+    hs = [vp(), vp()]
+    dev = torch.cuda.current_device()
+    try:
+        for h in hs:
+            abi_check(abi, abi.bml_dev_create(n, dev, ctypes.byref(h)), "create")
+            abi_check(abi, abi.bml_dev_configure(h, args.block, args.strip), "configure")
+        host_in = torch.frombuffer(bytearray(grid.to_bytes()), dtype=torch.uint8).pin_memory()
+        host_out = [torch.empty(n * n, dtype=torch.uint8).pin_memory() for _ in hs]
+
+        def job(i):
+            h = hs[i % 2]
+            abi_check(abi, abi.bml_dev_upload_async(h, vp(host_in.data_ptr()), n), "upload_async")
+            abi_check(abi, abi.bml_dev_step(h, steps, None, None, None, None), "step")
+            abi_check(abi, abi.bml_dev_download_async(h, vp(host_out[i % 2].data_ptr()), n), "download_async")
+
+        for i in range(max(2, args.warmup)):
+            job(i)
+        for h in hs:
+            abi_check(abi, abi.bml_dev_sync(h), "sync")
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            job(i)
+        for h in hs:
+            abi_check(abi, abi.bml_dev_sync(h), "sync")
+        total = time.perf_counter() - t0
+        check = check_result(bml, n, bytes(host_out[(args.steps - 1) % 2].numpy()), golden, steps)
+        return {"value": n * n * steps * args.steps / total / 1e9, "unit": "Gcell-updates/s",
+                "h2d_bytes_per_step": n * n, "d2h_bytes_per_step": n * n,
+                "ms_per_step": total / args.steps * 1e3,
+                "path": "C-ABI bml_dev_upload_async/step/download_async, two handles on two streams, "
+                        "pinned host buffers, jobs pipelined (transfers of one overlap stepping of the other)",
+                "result_check": check}
+    finally:
+        for h in hs:
+            if h:
+                abi.bml_dev_destroy(h)
+
+
 def run_e2e(abi, torch, bml, grid, n, steps, args, golden):
     vp = ctypes.c_void_p
     h = vp()
@@ -535,17 +594,12 @@ def run_e2e(abi, torch, bml, grid, n, steps, args, golden):
             times.append(time.perf_counter() - t0)
         # what was timed is checked against the UNMODIFIED reference: the downloaded
         # lattice's host grid_digest equals the golden (when one exists at `steps`)
-        check = None
-        if golden is not None and golden["steps"] == steps:
-            d = bml.Grid.from_bytes(n, bytes(host_out.numpy())).digest()
-            check = {"golden": golden["file"], "digest": f"0x{d:016x}",
-                     "match": f"0x{d:016x}" == golden["final_digest"]}
-            assert check["match"], f"e2e result differs from the reference golden: {check}"
+        check = check_result(bml, n, bytes(host_out.numpy()), golden, steps)
         total = sum(times)
         return {"value": n * n * steps * len(times) / total / 1e9, "unit": "Gcell-updates/s",
                 "h2d_bytes_per_step": n * n, "d2h_bytes_per_step": n * n,
                 "ms_per_step": total / len(times) * 1e3,
-                "path": "C-ABI bml_dev_upload/step/download, pinned host buffers",
+                "path": "C-ABI bml_dev_upload/step/download, pinned host buffers, one call at a time",
                 "result_check": check}
     finally:
         abi.bml_dev_destroy(h)

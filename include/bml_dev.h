@@ -92,6 +92,15 @@ int bml_dev_init_random(bml_dev *dev, double rho, uint64_t seed);
  * fix-up path at small n. reject_mask = 0 is exactly bml_dev_init_random. */
 int bml_dev_init_random_masked(bml_dev *dev, double rho, uint64_t seed, uint64_t reject_mask);
 
+/* Asynchronous forms: the same copies and (un)packing, enqueued on the handle's
+ * stream without waiting. `src` / `dst` must stay valid (pinned host memory for
+ * real overlap) until bml_dev_sync(), which also reports an invalid cell of an
+ * asynchronous upload (BML_EINVAL). With bml_dev_step (no metrics, also
+ * asynchronous) this lets a caller overlap one lattice's transfers with another
+ * handle's stepping; bench.py's e2e leg pipelines two handles this way. */
+int bml_dev_upload_async(bml_dev *dev, const uint8_t *src, size_t src_pitch);
+int bml_dev_download_async(bml_dev *dev, uint8_t *dst, size_t dst_pitch);
+
 /* One phase (step_phase). `moved` (nullable) receives the vehicles that
  * advanced (moved_in_phase). Single-band handles only. */
 int bml_dev_phase(bml_dev *dev, int phase, int64_t *moved);

@@ -347,6 +347,10 @@ cudaError_t enqueue_error_readback(bml_dev* d) {
 
 int errors_after_sync(bml_dev* d) {
     const int* h = d->err_host;
+    if (h[0]) {  // an asynchronous upload met a cell value outside {0, 1, 2}
+        cudaMemsetAsync(d->err, 0, sizeof(int), d->stream);
+        return fail(BML_EINVAL, "upload: cell value outside {0,1,2}");
+    }
     if (h[1]) {
         cudaMemsetAsync(d->err, 0, 4 * sizeof(int), d->stream);
         return fail(BML_ECUDA, h[1] == 3 ? "resident kernel: DSMEM handoff timed out"
@@ -851,14 +855,15 @@ int bml_dev_kernel_stats(bml_dev* d, int64_t* launches, double* kernel_ms, int r
     return BML_OK;
 }
 
-int bml_dev_upload(bml_dev* d, const uint8_t* src, size_t src_pitch) {
-    if (int rc = check(d)) return rc;
-    if (!src) return fail(BML_EINVAL, "bml_dev_upload: src is null");
-    if (src_pitch < static_cast<size_t>(d->n))
-        return fail(BML_EINVAL, "bml_dev_upload: pitch smaller than a row");
-    BML_CUDA(cudaMemsetAsync(d->err, 0, 4 * sizeof(int), d->stream));
-    BML_CUDA(cudaMemcpy2DAsync(d->staging, d->n, src, src_pitch, d->n, d->rows,
-                               cudaMemcpyDefault, d->stream));
+namespace {
+
+// H2D into the staging rows, then bit-pack (and the single band's ghost-row
+// images), all enqueued on the handle's stream. Invalid cells set err[0].
+int enqueue_upload(bml_dev* d, const uint8_t* src, size_t src_pitch, const char* who) {
+    if (!src) return fail(BML_EINVAL, std::string(who) + ": src is null");
+    if (src_pitch < static_cast<size_t>(d->n)) return fail(BML_EINVAL, std::string(who) + ": pitch smaller than a row");
+    BML_CUDA(cudaMemsetAsync(d->err, 0, sizeof(int), d->stream));
+    BML_CUDA(cudaMemcpy2DAsync(d->staging, d->n, src, src_pitch, d->n, d->rows, cudaMemcpyDefault, d->stream));
     const long long total = static_cast<long long>(d->rows) * d->W;
     pack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, d->stream>>>(
         d->staging, d->n, d->row0(d->cur), d->n, d->W, d->pitch, d->rows, d->err);
@@ -866,26 +871,50 @@ int bml_dev_upload(bml_dev* d, const uint8_t* src, size_t src_pitch) {
     if (d->single_band()) {
         if (int rc = fill_images(d, d->cur)) return rc;
     }
-    BML_CUDA(enqueue_error_readback(d));
-    BML_CUDA(cudaStreamSynchronize(d->stream));
-    if (d->err_host[0]) return fail(BML_EINVAL, "bml_dev_upload: cell value outside {0,1,2}");
     return BML_OK;
 }
 
-int bml_dev_download(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
-    if (int rc = check(d)) return rc;
-    if (!dst) return fail(BML_EINVAL, "bml_dev_download: dst is null");
-    if (dst_pitch < static_cast<size_t>(d->n))
-        return fail(BML_EINVAL, "bml_dev_download: pitch smaller than a row");
+int enqueue_download(bml_dev* d, uint8_t* dst, size_t dst_pitch, const char* who) {
+    if (!dst) return fail(BML_EINVAL, std::string(who) + ": dst is null");
+    if (dst_pitch < static_cast<size_t>(d->n)) return fail(BML_EINVAL, std::string(who) + ": pitch smaller than a row");
     const long long total = static_cast<long long>(d->rows) * d->W;
     unpack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, d->stream>>>(
         d->row0(d->cur), d->staging, d->n, d->n, d->W, d->pitch, d->rows);
     BML_CUDA(cudaGetLastError());
-    BML_CUDA(cudaMemcpy2DAsync(dst, dst_pitch, d->staging, d->n, d->n, d->rows,
-                               cudaMemcpyDefault, d->stream));
+    BML_CUDA(cudaMemcpy2DAsync(dst, dst_pitch, d->staging, d->n, d->n, d->rows, cudaMemcpyDefault, d->stream));
+    return BML_OK;
+}
+
+}  // namespace
+
+int bml_dev_upload(bml_dev* d, const uint8_t* src, size_t src_pitch) {
+    if (int rc = check(d)) return rc;
+    if (int rc = enqueue_upload(d, src, src_pitch, "bml_dev_upload")) return rc;
+    BML_CUDA(enqueue_error_readback(d));
+    BML_CUDA(cudaStreamSynchronize(d->stream));
+    if (d->err_host[0]) {
+        cudaMemsetAsync(d->err, 0, sizeof(int), d->stream);
+        return fail(BML_EINVAL, "bml_dev_upload: cell value outside {0,1,2}");
+    }
+    return errors_after_sync(d);
+}
+
+int bml_dev_download(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
+    if (int rc = check(d)) return rc;
+    if (int rc = enqueue_download(d, dst, dst_pitch, "bml_dev_download")) return rc;
     BML_CUDA(enqueue_error_readback(d));  // one synchronisation for data and flags
     BML_CUDA(cudaStreamSynchronize(d->stream));
     return errors_after_sync(d);
+}
+
+int bml_dev_upload_async(bml_dev* d, const uint8_t* src, size_t src_pitch) {
+    if (int rc = check(d)) return rc;
+    return enqueue_upload(d, src, src_pitch, "bml_dev_upload_async");
+}
+
+int bml_dev_download_async(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
+    if (int rc = check(d)) return rc;
+    return enqueue_download(d, dst, dst_pitch, "bml_dev_download_async");
 }
 
 int bml_dev_init_random_masked(bml_dev* d, double rho, uint64_t seed, uint64_t reject_mask) {
