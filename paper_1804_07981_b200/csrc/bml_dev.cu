@@ -46,6 +46,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "bml_dev.h"
 #include "bml_digest.cuh"
 #include "bml_init.cuh"
@@ -79,6 +81,25 @@ int cuda_fail(cudaError_t e, const char* what) {
         cudaError_t e_ = (call);                        \
         if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
     } while (0)
+
+// NVTX ranges ("bml" domain) around every C-ABI entry that enqueues device work,
+// so an nsys / ncu --nvtx timeline shows upload, stepping, halo exchange and
+// readback per band. Header-only NVTX v3: a no-op unless a tool is attached.
+nvtxDomainHandle_t nvtx_domain() {
+    static nvtxDomainHandle_t d = nvtxDomainCreateA("bml");
+    return d;
+}
+struct NvtxRange {
+    explicit NvtxRange(const char* what) {
+        nvtxEventAttributes_t e{};
+        e.version = NVTX_VERSION;
+        e.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+        e.messageType = NVTX_MESSAGE_TYPE_ASCII;
+        e.message.ascii = what;
+        nvtxDomainRangePushEx(nvtx_domain(), &e);
+    }
+    ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+};
 
 // ------------------------------------------------------------ dispatch table
 using StepKernel = void (*)(const StepArgs);
@@ -888,6 +909,7 @@ int enqueue_download(bml_dev* d, uint8_t* dst, size_t dst_pitch, const char* who
 }  // namespace
 
 int bml_dev_upload(bml_dev* d, const uint8_t* src, size_t src_pitch) {
+    const NvtxRange nvtx_range("bml_dev_upload");
     if (int rc = check(d)) return rc;
     if (int rc = enqueue_upload(d, src, src_pitch, "bml_dev_upload")) return rc;
     BML_CUDA(enqueue_error_readback(d));
@@ -900,6 +922,7 @@ int bml_dev_upload(bml_dev* d, const uint8_t* src, size_t src_pitch) {
 }
 
 int bml_dev_download(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
+    const NvtxRange nvtx_range("bml_dev_download");
     if (int rc = check(d)) return rc;
     if (int rc = enqueue_download(d, dst, dst_pitch, "bml_dev_download")) return rc;
     BML_CUDA(enqueue_error_readback(d));  // one synchronisation for data and flags
@@ -908,16 +931,19 @@ int bml_dev_download(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
 }
 
 int bml_dev_upload_async(bml_dev* d, const uint8_t* src, size_t src_pitch) {
+    const NvtxRange nvtx_range("bml_dev_upload_async");
     if (int rc = check(d)) return rc;
     return enqueue_upload(d, src, src_pitch, "bml_dev_upload_async");
 }
 
 int bml_dev_download_async(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
+    const NvtxRange nvtx_range("bml_dev_download_async");
     if (int rc = check(d)) return rc;
     return enqueue_download(d, dst, dst_pitch, "bml_dev_download_async");
 }
 
 int bml_dev_init_random_masked(bml_dev* d, double rho, uint64_t seed, uint64_t reject_mask) {
+    const NvtxRange nvtx_range("bml_dev_init_random");
     if (int rc = check(d)) return rc;
     if (!(rho >= 0.0 && rho <= 1.0))
         return fail(BML_EINVAL, "init_grid: density must be in [0, 1]");
@@ -961,6 +987,7 @@ int bml_dev_encode_ppm(bml_dev* d, uint8_t* dst, size_t dst_pitch) {
 }
 
 int bml_dev_digest_segment(bml_dev* d, uint64_t seg[6]) {
+    const NvtxRange nvtx_range("bml_dev_digest_segment");
     if (int rc = check(d)) return rc;
     if (!seg) return fail(BML_EINVAL, "bml_dev_digest_segment: seg is null");
     std::string msg;
@@ -991,6 +1018,7 @@ int bml_digest_finish(const uint64_t* segs, int count, uint64_t* digest) {
 }
 
 int bml_dev_counts(bml_dev* d, int64_t* lr, int64_t* tb) {
+    const NvtxRange nvtx_range("bml_dev_counts");
     if (int rc = check(d)) return rc;
     BML_CUDA(cudaMemsetAsync(d->scratch, 0, 2 * sizeof(unsigned long long), d->stream));
     counts_kernel<<<d->sms * 4, 256, 0, d->stream>>>(d->row0(d->cur), d->W, d->pitch, d->rows,
@@ -1087,6 +1115,7 @@ int run_segment(bml_dev* d, long long from, long long seg, bool count, bool ever
 
 int bml_dev_step(bml_dev* d, int64_t steps, int64_t* lr_moved, int64_t* tb_moved,
                  int64_t* lr_count, int64_t* tb_count) {
+    const NvtxRange nvtx_range("bml_dev_step");
     if (int rc = check(d)) return rc;
     if (steps < 0) return fail(BML_EINVAL, "bml_dev_step: steps must be >= 0");
     if (!d->single_band() && !d->connected)
@@ -1280,6 +1309,7 @@ int bml_dev_connect_local(bml_dev* d, bml_dev* up, bml_dev* down) {
 }
 
 int bml_dev_exchange_halos(bml_dev* d) {
+    const NvtxRange nvtx_range("bml_dev_exchange_halos");
     if (int rc = check(d)) return rc;
     if (!d->connected && !d->single_band())
         return fail(BML_EINVAL, "bml_dev_exchange_halos: a partial row band must be connected first");

@@ -201,8 +201,15 @@ step_block_kernel(const StepArgs a) {
     // the next grid items to warp 1, ..., so a launch with fewer items than
     // warps still spreads them evenly over the SMs and their sub-partitions.
     for (int item = (threadIdx.x >> 5) * gridDim.x + blockIdx.x; item < a.items; item += warps_total) {
-        const int strip = item / a.ncols;
-        const int col = item - strip * a.ncols;
+        const int order = item / a.ncols;
+        const int col = item - order * a.ncols;
+        // connected bands run boundary-first: the band's top and bottom strips are
+        // items of the first round, so both neighbours' ghost rows are published
+        // early and the interior strips overlap their wait (order 0 -> strip 0,
+        // order 1 -> the last strip, order k -> strip k-1)
+        const int strip = (a.single_band || a.nstrips < 2 || order == 0)
+                              ? order
+                              : (order == 1 ? a.nstrips - 1 : order - 1);
         StripCtx c;
         c.lane = lane;
         // rows split evenly: strip i owns [i*rows/nstrips, (i+1)*rows/nstrips)

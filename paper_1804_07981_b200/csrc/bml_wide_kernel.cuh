@@ -212,8 +212,15 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
     uint32_t phase_bits = 0;  // bit i: parity of slot i's next completion
 
     for (int item = wid * gridDim.x + blockIdx.x; item < a.items; item += warps_total) {
-        const int strip = item / a.ncols;
-        const int col = item - strip * a.ncols;
+        const int order = item / a.ncols;
+        const int col = item - order * a.ncols;
+        // connected bands run boundary-first: the band's top and bottom strips are
+        // items of the first round, so both neighbours' ghost rows are published
+        // early and the interior strips overlap their wait (order 0 -> strip 0,
+        // order 1 -> the last strip, order k -> strip k-1)
+        const int strip = (a.single_band || a.nstrips < 2 || order == 0)
+                              ? order
+                              : (order == 1 ? a.nstrips - 1 : order - 1);
         WideCtx c;
         c.lane = lane;
         c.r_lo = static_cast<int>(static_cast<long long>(strip) * a.rows / a.nstrips);

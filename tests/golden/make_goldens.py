@@ -15,6 +15,7 @@ GPU box (which has no /root/reference) can check the CUDA path against it.
                                                    # N=65536, 10000 steps as ten resumable 1000-step
                                                    # legs (golden leg, then `file` legs on the dumped
                                                    # lattice); same digest as `c4`, restartable
+    python tests/golden/make_goldens.py chain N RHO STEPS LEG WORKDIR   # any size, same scheme
 
 Every record holds the reference's init digest, final digest after `steps`
 full steps, the vehicle counts and (where metrics=1) the observer-path sums
@@ -142,6 +143,10 @@ if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "small"
     if which == "c4chain":
         run_chain(65536, 0.35, 1, 10000, 1000, sys.argv[2])
+        sys.exit(0)
+    if which == "chain":  # chain N RHO STEPS LEG WORKDIR (e.g. the weak-sweep sizes 23168, 46336)
+        n, rho, steps, leg, work = sys.argv[2:7]
+        run_chain(int(n), float(rho), 1, int(steps), int(leg), work)
         sys.exit(0)
     if which == "regimes":
         run_regimes()

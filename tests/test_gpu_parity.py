@@ -382,3 +382,34 @@ def test_seam_mode_bands_and_metrics(gpu, oracle, n, bands):
     assert final.to_bytes() == want
     assert [m.lr_moved for m in metrics] == lm and [m.tb_moved for m in metrics] == tm
     assert [m.lr_count for m in metrics] == lc and [m.tb_count for m in metrics] == tc
+
+
+# ----------------------------------------------------------- the benched instantiations
+def test_bare_loop_golden_c1(gpu):
+    """configs[1] exactly as bench.py runs it: the bare loop (no metrics) of 4096 steps,
+    through the resident kernel (COUNT=0) and through the streaming kernel, against the
+    unmodified reference's final digest."""
+    g = [x for x in load_goldens() if x["n"] == 1024 and x["steps"] == 4096][0]
+    grid = gpu.init_grid(1024, g["rho"], g["seed"])
+    for resident in (1, 0):
+        lat = gpu.DeviceLattice(1024)
+        lat.set_resident(resident)
+        lat.upload(grid)
+        lat.step(g["steps"])
+        assert (lat.resident_cluster > 0) == bool(resident)
+        assert f"0x{lat.digest():016x}" == g["final_digest"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("bands", [2, 4, 8])
+@pytest.mark.parametrize("g", [g for g in load_goldens() if g["n"] > 8192], ids=_golden_ids)
+def test_reference_golden_huge_row_bands(gpu, g, bands):
+    """configs[3]/[4] goldens through `bands` row bands of ceil(N/g) rows (one GPU,
+    in-kernel ghost-row exchange between the bands' buffers): the literal multi-GPU
+    split, bit-exact with the unmodified reference."""
+    lat = gpu.DeviceLattice(g["n"], bands)
+    lat.init_random(g["rho"], g["seed"])
+    assert f"0x{lat.digest():016x}" == g["init_digest"]
+    lat.step(g["steps"])
+    assert f"0x{lat.digest():016x}" == g["final_digest"]
+    assert lat.counts() == (g["lr_count"], g["tb_count"])
