@@ -318,7 +318,9 @@ def run_reference_impl(args, wl):
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic (reference init_grid seed)",
-        "config": config_block(args, desc, n, rho, seed, steps, args.gpus),
+        "config": {"workload": config_block(args, desc, n, rho, seed, steps, args.gpus)["workload"],
+                   "n": n, "rho": rho, "seed": seed, "steps_per_run": steps, "scaling_mode": args.scaling,
+                   "parallelism": "host CPU (reference backends; rank 0 only)"},
         "cpu_baseline": cpu_baseline_record(res, steps, reps),
         "e2e": {"value": value, "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},

@@ -157,11 +157,10 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
             if (static_cast<unsigned>(rho - c.r_lo) < span) q.cm[s] += __popc(L & ~nextO & c.valid);
             if (static_cast<unsigned>(rho - 1 - c.r_lo) < span) {
                 q.cm[s] += static_cast<uint32_t>(__popc(tB & ~Op & c.valid)) << 16;
-                // vehicle census of the emitted row: after every step (COUNT 2: row
+                // vehicle census of the emitted row after every step (COUNT 2: row
                 // bands, whose counts change as TB vehicles cross band edges, and the
-                // strict single-band mode), or only after the launch's last step
-                // (COUNT 1: the census at launch boundaries, one row in K stages)
-                if (COUNT == 2 || s == K - 1)
+                // strict single-band mode); COUNT 1 takes it at the store below
+                if (COUNT == 2)
                     q.cc[s] += __popc(newL & c.valid) +
                                (static_cast<uint32_t>(__popc(newT & c.valid)) << 16);
             }
@@ -172,6 +171,15 @@ __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const 
             q.nt[s][P3] = newT;
         } else {
             store_row<MODE>(a, c, j - 2 * K + 1, newL, newT);
+            if (COUNT == 1) {  // census after the launch's last step: the stored row
+                // (aligned modes store whole words: span is 0 for ghost lanes, so the
+                // stored-row test alone selects the counted cells; branch-free select)
+                const bool st = static_cast<unsigned>(j - 2 * K + 1 - c.r_lo) < c.span;
+                const uint32_t cl = MODE == kAligned || MODE == kFullRow ? newL : (newL & c.valid);
+                const uint32_t ct = MODE == kAligned || MODE == kFullRow ? newT : (newT & c.valid);
+                const uint32_t add = __popc(cl) + (static_cast<uint32_t>(__popc(ct)) << 16);
+                q.cc[K - 1] += st ? add : 0u;
+            }
         }
     }
 }

@@ -145,14 +145,23 @@ __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const 
             if (static_cast<unsigned>(rho - 1 - c.r_lo) < span) {
                 q.cm[s] += static_cast<uint32_t>(__popc(tB[0] & ~Op[0] & c.v0) + __popc(tB[1] & ~Op[1] & c.v1))
                            << 16;
-                if (COUNT == 2 || s == K - 1) {
+                if (COUNT == 2) {
                     const uint32_t* nl = q.lp[s][(P2 + 1) % 2];
                     q.cc[s] += __popc(nl[0] & c.v0) + __popc(nl[1] & c.v1) +
                                (static_cast<uint32_t>(__popc(newT[0] & c.v0) + __popc(newT[1] & c.v1)) << 16);
                 }
             }
         }
-        if (s == K - 1) wide_store(a, c, j - 2 * K + 1, q.lp[s][(P2 + 1) % 2], newT);
+        if (s == K - 1) {
+            const uint32_t* nl = q.lp[s][(P2 + 1) % 2];
+            wide_store(a, c, j - 2 * K + 1, nl, newT);
+            if (COUNT == 1) {  // census after the launch's last step: the stored row (branch-free)
+                const bool st = static_cast<unsigned>(j - 2 * K + 1 - c.r_lo) < c.span;
+                const uint32_t add = __popc(nl[0] & c.v0) + __popc(nl[1] & c.v1) +
+                                     (static_cast<uint32_t>(__popc(newT[0] & c.v0) + __popc(newT[1] & c.v1)) << 16);
+                q.cc[K - 1] += st ? add : 0u;
+            }
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             q.oc[s][h] = Op[h];

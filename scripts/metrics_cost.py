@@ -1,6 +1,6 @@
 """Cost of the fused per-step metrics: DeviceLattice.step vs
-step_with_metrics (lr/tb moved + counts every step, conservation checked) on the same
-lattice. Prints one JSON line per size."""
+step_with_metrics (lr/tb moved every step + the vehicle census: at launch boundaries by
+default, after every step with set_census(True)) on the same lattice. One JSON line per size."""
 import json
 import time
 
@@ -20,11 +20,16 @@ for n, steps in ((1024, 4096), (8192, 2000), (32768, 400)):
     lat.step(steps)
     lat.synchronize()
     bare = time.perf_counter() - t
-    lat.step_with_metrics(steps)
-    t = time.perf_counter()
-    m = lat.step_with_metrics(steps)
-    with_m = time.perf_counter() - t
     cu = n * n * steps
-    print(json.dumps({"n": n, "steps": steps, "bare_tcups": cu / bare / 1e12,
-                      "metrics_tcups": cu / with_m / 1e12, "slowdown": with_m / bare,
-                      "last_mobility": m[-1].mobility}), flush=True)
+    rec = {"n": n, "steps": steps, "bare_tcups": cu / bare / 1e12}
+    for strict in (False, True):
+        lat.set_census(strict)
+        lat.step_with_metrics(steps)
+        t = time.perf_counter()
+        m = lat.step_with_metrics(steps)
+        with_m = time.perf_counter() - t
+        key = "strict" if strict else "boundary"
+        rec[f"metrics_{key}_tcups"] = cu / with_m / 1e12
+        rec[f"slowdown_{key}"] = with_m / bare
+    rec["last_mobility"] = m[-1].mobility
+    print(json.dumps(rec), flush=True)
