@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, nargs="+", default=[65536, 32768])
 ap.add_argument("--bands", type=int, nargs="+", default=[1, 2, 4, 8])
 ap.add_argument("--launches", type=int, default=16)
+ap.add_argument("--block", type=int, default=16, help="steps per band launch")
 args = ap.parse_args()
 
 lib = ctypes.CDLL(bml.LIB_DEV)
@@ -37,18 +38,18 @@ for n in args.n:
     ref_digest = None
     for g in args.bands:
         lat = bml.DeviceLattice(n, g)
-        lat.configure(block_steps=16, strip_rows=0)
+        lat.configure(block_steps=args.block, strip_rows=0)
         lat.init_random(0.35, 1)
         hs = [vp(lat.handle(b)) for b in range(g)]
         for h in hs:  # warm-up launch per band
-            assert lib.bml_dev_step(h, 16, None, None, None, None) == 0
+            assert lib.bml_dev_step(h, args.block, None, None, None, None) == 0
             assert lib.bml_dev_sync(h) == 0
         for h in hs:
             lib.bml_dev_enable_timing(h, 1)
             lib.bml_dev_kernel_stats(h, None, None, 1)
         for _ in range(args.launches):
             for h in hs:
-                assert lib.bml_dev_step(h, 16, None, None, None, None) == 0
+                assert lib.bml_dev_step(h, args.block, None, None, None, None) == 0
                 assert lib.bml_dev_sync(h) == 0
         per_band = []
         for h in hs:
@@ -60,8 +61,8 @@ for n in args.n:
         d = lat.digest()
         ref_digest = d if ref_digest is None else ref_digest
         worst = max(per_band)  # the slowest band sets the pace of a lockstep multi-GPU run
-        per_gpu_tcups = n * ((n + g - 1) // g) * 16 / (worst / 1e3) / 1e12
-        rec = {"n": n, "bands": g, "band_rows": (n + g - 1) // g, "ms_per_launch_max": worst,
+        per_gpu_tcups = n * ((n + g - 1) // g) * args.block / (worst / 1e3) / 1e12
+        rec = {"n": n, "bands": g, "block": args.block, "band_rows": (n + g - 1) // g, "ms_per_launch_max": worst,
                "ms_per_launch_mean": sum(per_band) / g, "per_gpu_tcups": per_gpu_tcups,
                "projected_total_tcups": per_gpu_tcups * g, "geometry_band0": [x.value for x in geo],
                "digest_equal": d == ref_digest}
