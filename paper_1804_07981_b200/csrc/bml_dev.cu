@@ -40,6 +40,7 @@
 #include <mutex>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -57,6 +58,7 @@
 #include "bml_step_kernel.cuh"
 #include "bml_support_kernels.cuh"
 #include "bml_wide_kernel.cuh"
+#include "bml_split_kernel.cuh"
 
 using namespace bml_k;  // the kernels and their helpers (bml_kernels_common.cuh and friends)
 
@@ -153,6 +155,15 @@ StepKernel pick_wide(int k, int count, bool tma = true) {
     return nullptr;
 }
 
+// stage-split kernel (a warp pair per item, bml_split_kernel.cuh): aligned rows, K = 16
+constexpr int kSplitMaxThreads = 384;  // 6 pairs per CTA at <= 168 registers
+StepKernel pick_split(int k, int mode, int count) {
+    if (k != 16 || mode != kAligned) return nullptr;
+    return count == 2 ? step_split_kernel<16, kAligned, 2, kSplitMaxThreads>
+           : count     ? step_split_kernel<16, kAligned, 1, kSplitMaxThreads>
+                       : step_split_kernel<16, kAligned, 0, kSplitMaxThreads>;
+}
+
 // count: 0 no metrics, 1 moved counts, 2 moved counts + vehicle census
 StepKernel pick(int k, int mode, int count) {
     if (mode == kFullRow)
@@ -236,10 +247,14 @@ struct bml_dev {
     bool single_band() const { return rows == n && row_begin == 0; }
     // the wide-lane kernel: aligned rows of >= 64 words, an even word count
     bool wide_ok() const { return mode == kAligned && W >= 64 && W % 2 == 0; }
-    bool use_wide() const { return variant != 1 && wide_ok() && (variant >= 2 || wide_auto()); }
+    bool use_wide() const {
+        return wide_ok() && ((variant >= 2 && variant <= 4) || (variant == 0 && wide_auto()));
+    }
     // steps per wide launch for a metrics mode (0 = bare loop)
     int wide_depth(int metrics) const { return metrics == 0 && variant != 3 ? 14 : 12; }
     bool wide_auto() const { return false; }
+    // the stage-split kernel (a warp pair per item): aligned rows; variant 5
+    bool use_split() const { return variant == 5 && mode == kAligned; }
     int ncols() const { return use_wide() ? (W + kWideOut - 1) / kWideOut : narrow_ncols(); }
     int narrow_ncols() const {
         if (mode == kFullRow) return 1;
@@ -327,6 +342,12 @@ int create_common(int n, int row_begin, int row_end, int device, bml_dev** out) 
     const int nb = n - 32 * (d->W - 1);
     d->last_mask = nb == 32 ? kFull : ((1u << nb) - 1u);
     d->mode = (n % 32 != 0) ? (d->W >= 32 ? kSeam : kGeneric) : (d->W == 32 ? kFullRow : kAligned);
+    // BML_VARIANT (tuning / experiments): the streaming-kernel variant new handles
+    // start with, so row bands built inside DeviceLattice get it before connecting
+    if (const char* v = std::getenv("BML_VARIANT")) {
+        const int iv = std::atoi(v);
+        if (iv >= 0 && iv <= 5) d->variant = iv;
+    }
     cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, device);
 
     auto bail = [&](cudaError_t err, const char* what) {
@@ -430,15 +451,26 @@ int choose_nstrips(const bml_dev* d, int k, int warps_per_sm, int ncols) {
 int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int metrics_stride) {
     const int metrics = count ? (census ? 2 : 1) : 0;
     const bool wide = d->use_wide() && pick_wide(k, metrics);
-    StepKernel kern = wide ? pick_wide(k, metrics, d->variant != 4) : pick(k, d->mode, metrics);
+    const bool split = !wide && d->use_split() && pick_split(k, d->mode, metrics);
+    StepKernel kern = wide ? pick_wide(k, metrics, d->variant != 4)
+                      : split ? pick_split(k, d->mode, metrics)
+                              : pick(k, d->mode, metrics);
     if (!kern) return fail(BML_EINVAL, "unsupported block depth " + std::to_string(k));
     const int u_max = warps_per_smsp(kern);  // 3 at <= 168 registers/thread
     // every strip has >= min(strip_rows, 16) rows, so for connected bands the
     // ghost-row sources of a band never straddle strips
     // the model scans every strip count: memoised per (k, strip setting)
     if (d->ns_cache_k[k] <= 0 || d->ns_cache_setting[k] != d->strip_rows) {
-        d->ns_cache_k[k] = choose_nstrips(d, k, 4 * (wide ? std::min(2, u_max) : u_max),
-                                          wide ? d->ncols() : d->narrow_ncols());
+        if (split && d->strip_rows == 0) {
+            // one item per warp pair, kSplitMaxThreads / 64 pairs per SM
+            const int cols = d->narrow_ncols();
+            const int want = d->sms * (kSplitMaxThreads / 64);
+            const int max_strips = std::max(1, d->rows / (d->connected ? kHalo : 1));
+            d->ns_cache_k[k] = std::max(1, std::min(max_strips, want / cols));  // one round: items <= want
+        } else {
+            d->ns_cache_k[k] = choose_nstrips(d, k, 4 * (wide ? std::min(2, u_max) : u_max),
+                                              wide ? d->ncols() : d->narrow_ncols());
+        }
         d->ns_cache_setting[k] = d->strip_rows;
     }
     int nstrips = d->ns_cache_k[k];
@@ -489,8 +521,10 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
     // one CTA per SM with 4u warps, u = the warps per SMSP the items need
     const int u = std::min(wide ? 2 : u_max, std::max(1, (a.items + 4 * d->sms - 1) / (4 * d->sms)));
     const int grid = std::max(1, std::min(d->sms, a.items));
-    const int threads = 4 * u * 32;
-    if (u <= 2 && !wide) {
+    // split: threads = 64 per warp pair, one pair per item per CTA round
+    const int threads = split ? 64 * std::min(kSplitMaxThreads / 64, std::max(1, (a.items + d->sms - 1) / d->sms))
+                              : 4 * u * 32;
+    if (u <= 2 && !wide && !split) {
         if (StepKernel narrow = pick_narrow(k, d->mode, metrics)) kern = narrow;
     }
     d->last_nstrips = nstrips;
@@ -821,7 +855,7 @@ int bml_dev_set_resident(bml_dev* d, int mode) {
 
 int bml_dev_set_variant(bml_dev* d, int variant) {
     if (int rc = check(d)) return rc;
-    if (variant < 0 || variant > 4) return fail(BML_EINVAL, "bml_dev_set_variant: 0 (auto), 1, 2, 3 or 4");
+    if (variant < 0 || variant > 5) return fail(BML_EINVAL, "bml_dev_set_variant: 0 (auto) .. 5");
     if (d->connected)
         return fail(BML_EINVAL, "bml_dev_set_variant: set before bml_dev_connect (all bands alike)");
     d->variant = variant;

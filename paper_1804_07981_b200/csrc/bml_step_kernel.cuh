@@ -114,13 +114,16 @@ __device__ __noinline__ void copy_images(const StepArgs& a, int r_lo, int r_hi, 
     }
 }
 
-template <int K, int MODE, int COUNT, int P>
+// Stages [S0, S1) of one pipeline iteration (the whole pipeline by default;
+// step_split_kernel runs the two halves in two warps). Stage S0 > 0 reads the
+// stage-(S0-1) state slots, which the caller fills.
+template <int K, int MODE, int COUNT, int P, int S0 = 0, int S1 = K>
 __device__ __forceinline__ void pipe_iter(PipeState<K>& q, const uint2 x, const int j,
                                           const StepArgs& a, StripCtx& c) {
     constexpr int P3 = P % 3, P2 = P % 2;
-    q.xt[P3] = x.y;
+    if (S0 == 0) q.xt[P3] = x.y;
 #pragma unroll
-    for (int s = K - 1; s >= 0; --s) {
+    for (int s = S1 - 1; s >= S0; --s) {
         const uint32_t L = (s == 0) ? x.x : q.lp[s > 0 ? s - 1 : 0][P2];
         const uint32_t T = (s == 0) ? x.y : q.nt[s > 0 ? s - 1 : 0][(P3 + 2) % 3];
         const uint32_t tB = (s == 0) ? q.xt[(P3 + 2) % 3] : q.nt[s > 0 ? s - 1 : 0][(P3 + 1) % 3];

@@ -92,3 +92,51 @@ def test_wide_variant_row_bands(gpu, oracle):
     finally:
         for h in hs:
             lib.bml_dev_destroy(h)
+
+
+# ----------------------------------------------------------- the stage-split kernel (variant 5)
+@pytest.mark.parametrize("n,steps", [(2048, 45), (4096, 37), (8192, 33)])
+def test_split_variant_matches_oracle(gpu, oracle, n, steps):
+    cells = oracle.init_grid(n, 0.36, n + 5)
+    lat = gpu.DeviceLattice(n)
+    set_variant(gpu, lat, 5)
+    lat.upload(gpu.Grid.from_bytes(n, cells))
+    lat.step(steps)
+    assert lat.download().to_bytes() == oracle.run(n, cells, steps)
+
+
+@pytest.mark.parametrize("strict", [False, True])
+def test_split_variant_metrics(gpu, oracle, strict):
+    n, steps = 2048, 40
+    cells = oracle.init_grid(n, 0.4, 6)
+    _, (lm, tm, lc, tc) = oracle.run(n, cells, steps, metrics=True)
+    lat = gpu.DeviceLattice(n)
+    set_variant(gpu, lat, 5)
+    lat.set_census(strict)
+    lat.upload(gpu.Grid.from_bytes(n, cells))
+    ms = lat.step_with_metrics(steps)
+    assert [m.lr_moved for m in ms] == lm and [m.tb_moved for m in ms] == tm
+    assert [m.lr_count for m in ms] == lc and [m.tb_count for m in ms] == tc
+
+
+def test_split_variant_row_bands_env(gpu, oracle):
+    """Row bands built by DeviceLattice with BML_VARIANT=5 in a subprocess (the
+    variant must be set before the bands connect)."""
+    import os
+    import subprocess
+    import sys
+
+    n, steps = 2048, 50
+    code = f"""
+import sys; sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import paper_1804_07981_b200 as bml
+lat = bml.DeviceLattice({n}, 4)
+lat.init_random(0.35, 3)
+lat.step({steps})
+print(hex(lat.digest()))
+"""
+    env = dict(os.environ, BML_VARIANT="5")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    cells = oracle.init_grid(n, 0.35, 3)
+    assert int(out.stdout.strip(), 16) == oracle.digest(n, oracle.run(n, cells, steps))
