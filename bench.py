@@ -643,6 +643,7 @@ def run_b200_multi(args, wl):
             dist.barrier()
     band.exchange_halos()
     band_cells = band.download_rows()  # host copy of the input, for the e2e leg
+    dist.barrier()  # every band's first ghost rows are published before anyone steps
     stream = torch.cuda.Stream(device=dev)
     band.set_stream(stream.cuda_stream)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
