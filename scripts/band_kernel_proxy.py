@@ -23,6 +23,7 @@ ap.add_argument("--n", type=int, nargs="+", default=[65536, 32768])
 ap.add_argument("--bands", type=int, nargs="+", default=[1, 2, 4, 8])
 ap.add_argument("--launches", type=int, default=16)
 ap.add_argument("--block", type=int, default=16, help="steps per band launch")
+ap.add_argument("--strips", type=int, nargs="+", default=[0], help="-ns per band (0 = automatic)")
 args = ap.parse_args()
 
 lib = ctypes.CDLL(bml.LIB_DEV)
@@ -36,9 +37,9 @@ lib.bml_dev_last_launch.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 3
 for n in args.n:
     single = None
     ref_digest = None
-    for g in args.bands:
+    for g, ns in [(g, ns) for g in args.bands for ns in args.strips]:
         lat = bml.DeviceLattice(n, g)
-        lat.configure(block_steps=args.block, strip_rows=0)
+        lat.configure(block_steps=args.block, strip_rows=-ns if ns > 1 else (-1 if ns == 0 else 65536))
         lat.init_random(0.35, 1)
         hs = [vp(lat.handle(b)) for b in range(g)]
         for h in hs:  # warm-up launch per band
@@ -62,11 +63,11 @@ for n in args.n:
         ref_digest = d if ref_digest is None else ref_digest
         worst = max(per_band)  # the slowest band sets the pace of a lockstep multi-GPU run
         per_gpu_tcups = n * ((n + g - 1) // g) * args.block / (worst / 1e3) / 1e12
-        rec = {"n": n, "bands": g, "block": args.block, "band_rows": (n + g - 1) // g, "ms_per_launch_max": worst,
+        rec = {"n": n, "bands": g, "block": args.block, "strips_requested": ns, "band_rows": (n + g - 1) // g, "ms_per_launch_max": worst,
                "ms_per_launch_mean": sum(per_band) / g, "per_gpu_tcups": per_gpu_tcups,
                "projected_total_tcups": per_gpu_tcups * g, "geometry_band0": [x.value for x in geo],
                "digest_equal": d == ref_digest}
-        if g == 1:
+        if g == 1 and single is None:
             single = per_gpu_tcups
         rec["per_gpu_efficiency_vs_single"] = per_gpu_tcups / single if single else None
         print(json.dumps(rec), flush=True)
