@@ -147,3 +147,35 @@ def test_partial_band_must_be_connected(gpu):
         assert lib.bml_dev_exchange_halos(h) == 1
     finally:
         lib.bml_dev_destroy(h)
+
+
+def _largest_block(remaining, cap=16):
+    k = 16
+    while k > 1 and (k > remaining or k > cap):
+        k >>= 1
+    return k
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_census_fault_fuzz(gpu, case):
+    """Seeded random lattices, step counts and fault steps: strict and resident census
+    report the step right after the fault; the streaming launch-boundary census reports
+    the end of the first launch after it (the call's launches split at the fault)."""
+    import random
+
+    rng = random.Random(1000 + case)
+    n = rng.choice([64, 96, 128, 200, 256, 333, 512, 1024, 1056, 2048])
+    steps = rng.randint(2, 90)
+    fault = rng.randint(0, steps - 1)
+    mode = rng.choice(["strict", "boundary"])
+    resident = rng.choice([0, 1])
+    lat = gpu.DeviceLattice(n)
+    lat.set_resident(resident)
+    lat.set_census(mode == "strict")
+    lat.upload(gpu.init_grid(n, rng.choice([0.2, 0.35, 0.5]), rng.randint(1, 99)))
+    lat.debug_fault(fault, rng.randrange(n), rng.randrange(n))
+    with pytest.raises(RuntimeError) as ei:
+        lat.step_with_metrics(steps)
+    per_step = mode == "strict" or lat.resident_cluster > 0
+    want = fault + 1 if per_step else fault + _largest_block(steps - fault)
+    assert violation_step(ei.value) == want, (n, steps, fault, mode, resident, lat.resident_cluster)
