@@ -188,6 +188,7 @@ def load_abi():
                                          ctypes.POINTER(ctypes.c_double), ctypes.c_int]
     lib.bml_dev_info.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 5 + [ctypes.POINTER(ctypes.c_size_t)]
     lib.bml_dev_last_launch.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 3
+    lib.bml_dev_last_kernel.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64)]
     lib.bml_dev_last_error.restype = ctypes.c_char_p
     return lib
 
@@ -205,20 +206,50 @@ def abi_check(lib, rc, what):
 
 
 # ---------------------------------------------------------------- reference CPU arm
+# Per kernel: ALU-pipe and issued warp-instructions per 32-cell stage (one lane,
+# one step) of the innermost row loop, counted in the SASS of the built library
+# (scripts/sass_inner_loop.py). The ALU pipe retires 2 and an SM
+# issues 4 warp-instructions per clock, and a warp-instruction covers 32 lanes, so
+# a bound is (2 or 4) / count x 1024 cell-updates per clock per SM.
+KERNEL_MIX = {
+    # 4 LOP3 + 2 funnel shifts (+ loop predicates); 1089 instructions / 96 stages
+    "step_block_kernel": {"alu": 6.0, "issue": 11.34},
+    # even/odd layout: 3.5 LOP3 + 1 funnel shift (+ predicates, selects); 1709 / 168 stages
+    "step_wide_kernel (even/odd layout)": {"alu": 4.8, "issue": 10.17},
+    "resident_kernel": {"alu": 6.0, "issue": None},
+}
+KERNEL_NAMES = {1: "step_block_kernel", 2: "step_wide_kernel", 3: "step_wide_kernel (even/odd layout)",
+                4: "step_split_kernel", 5: "resident_kernel"}
+
+
+def last_kernel(abi, h):
+    k, st = ctypes.c_int(), ctypes.c_int64()
+    abi_check(abi, abi.bml_dev_last_kernel(h, ctypes.byref(k), ctypes.byref(st)), "last_kernel")
+    return KERNEL_NAMES.get(k.value, "step_block_kernel")
+
+
 def alu_roofline(kernel, achieved_gcups, resident_cluster, sm_max_mhz, sms=148):
-    """The bound that actually limits the bit-plane kernels: the
-    ALU pipe. Per 32-cell stage the kernels issue 6 ALU-pipe instructions (4 LOP3
-    + 2 funnel shifts; the two ORs of disjoint planes go to the FMA pipe), and the
-    ALU pipe retires 2 warp-instructions per clock per SM: 2/6 x 1024 = 341
-    cell-updates per clock per SM. `achieved` is the dominant kernel's rate (its
-    event-timed launches), over the SMs it runs on (the resident kernel: one
-    cluster)."""
+    """The bound that actually limits the bit-plane kernels: the ALU
+    pipe or instruction issue, whichever is lower for the kernel's SASS mix
+    (KERNEL_MIX). The narrow kernel issues 6 ALU-pipe instructions per 32-cell
+    stage (4 LOP3 + 2 funnel shifts; the ORs of disjoint planes go to the FMA
+    pipe): 2/6 x 1024 = 341 cell-updates per clock per SM, below its issue bound.
+    The even/odd-layout kernel needs 4.8 ALU but issues 10.2 instructions per
+    stage, so issue binds: 4/10.17 x 1024 = 403. `achieved` is the dominant
+    kernel's rate (its event-timed launches), over the SMs it runs on (the
+    resident kernel: one cluster)."""
     used = resident_cluster if kernel == "resident_kernel" and resident_cluster else sms
     mhz = sm_max_mhz or 1965
-    peak = 2.0 / 6.0 * 1024 * used * mhz * 1e6 / 1e9
-    return {"bound": "alu", "achieved": achieved_gcups, "peak": peak, "unit": "Gcell-updates/s",
-            "frac": achieved_gcups / peak, "sms": used, "sm_mhz": mhz,
-            "alu_instructions_per_32_cell_stage": 6}
+    mix = KERNEL_MIX.get(kernel, KERNEL_MIX["step_block_kernel"])
+    alu_peak = 2.0 / mix["alu"] * 1024 * used * mhz * 1e6 / 1e9
+    issue_peak = 4.0 / mix["issue"] * 1024 * used * mhz * 1e6 / 1e9 if mix["issue"] else None
+    binding = "issue" if issue_peak and issue_peak < alu_peak else "alu"
+    peak = min(alu_peak, issue_peak) if issue_peak else alu_peak
+    return {"bound": binding, "achieved": achieved_gcups, "peak": peak, "unit": "Gcell-updates/s",
+            "frac": achieved_gcups / peak, "sms": used, "sm_mhz": mhz, "kernel": kernel,
+            "alu_peak": alu_peak, "issue_peak": issue_peak,
+            "alu_instructions_per_32_cell_stage": mix["alu"],
+            "issued_instructions_per_32_cell_stage": mix["issue"]}
 
 
 def cpu_sample_plan(n, steps, reps):
@@ -419,7 +450,7 @@ def run_b200(args, wl):
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
     kernel_share = kms.value / total_ms if total_ms else None
 
-    kernel = "resident_kernel" if lat.resident_cluster > 0 else "step_block_kernel"
+    kernel = "resident_kernel" if lat.resident_cluster > 0 else last_kernel(abi, h)
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tpath) and n == n1:
@@ -464,9 +495,10 @@ def run_b200(args, wl):
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": kernel, "peak_source": peak_src,
                      "frac_datasheet": achieved / DATASHEET_HBM_GBS,  # also vs 8 TB/s
-                     "binding_bound": "alu (see roofline_alu): temporal blocking keeps DRAM traffic "
-                                      "at ~1/16 of the 4 B/cell-update algorithmic figure",
-                     "launch_geometry": last_launch(abi, h) if kernel == "step_block_kernel" else None,
+                     "binding_bound": "alu pipe or instruction issue, whichever roofline_alu.bound names: "
+                                      "temporal blocking keeps DRAM traffic at ~1/14-1/16 of the 4 B/cell-update "
+                                      "algorithmic figure",
+                     "launch_geometry": last_launch(abi, h) if kernel.startswith("step_") else None,
                      "resident_cluster": lat.resident_cluster,
                      "algorithmic_bytes_per_cell_update": BYTES_PER_CELL_UPDATE,
                      "launches": launches.value, "avg_launch_us": avg_launch_ms * 1e3,
@@ -476,7 +508,9 @@ def run_b200(args, wl):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "parity": parity,
-        "gpu_launches": timed_launches,
+        # step kernels (kernel_stats) + the even/odd layout's two in-place
+        # conversion kernels per bml_dev_step call when that kernel ran
+        "gpu_launches": timed_launches + (2 * args.steps if "even/odd" in kernel else 0),
         "init": {"s": t_init, "where": "device" if n >= DEVICE_INIT_N else "host",
                  "note": "init_grid incl. readback into a host Grid; untimed input generation"},
         "wall_s": wall,

@@ -181,8 +181,26 @@ int bml_dev_debug_fault(bml_dev *dev, int64_t at_step, int row, int col);
 /* Streaming-kernel variant: 0 = automatic (default), 1 = narrow (32 cells per
  * lane, K <= 16 steps per launch), 2 / 3 = wide (64 cells per lane, TMA
  * bulk-copied rows, K = 14 / 12 steps per launch; n % 64 == 0 and n >= 2048
- * only, else narrow). Row bands: set on every band before connecting. */
+ * only, else narrow), 4 = wide with a per-lane cp.async row ring, 5 = stage-split
+ * (a warp pair per item), 6 = wide in the even/odd layout (each 64-cell group held
+ * as its even then its odd cells, 5 instead of 6 ALU instructions per 32 cells and
+ * step; the buffer is converted in place around bare-loop runs of >= 56 steps of a
+ * single band, n % 64 == 0, n >= 2048; anything else runs the narrow kernel).
+ * Row bands: set on every band before connecting. */
 int bml_dev_set_variant(bml_dev *dev, int variant);
+
+/* The step kernel that ran the most steps of the last bml_dev_step call, and
+ * how many: BML_KERNEL_NONE (no steps), _NARROW (step_block_kernel, 32 cells per
+ * lane), _WIDE (step_wide_kernel, 64 cells per lane), _WIDE_EO (step_wide_kernel
+ * in the even/odd layout), _SPLIT (step_split_kernel), _RESIDENT (the
+ * cluster-resident kernel). For reports (bench.py's roofline names it). */
+#define BML_KERNEL_NONE 0
+#define BML_KERNEL_NARROW 1
+#define BML_KERNEL_WIDE 2
+#define BML_KERNEL_WIDE_EO 3
+#define BML_KERNEL_SPLIT 4
+#define BML_KERNEL_RESIDENT 5
+int bml_dev_last_kernel(bml_dev *dev, int *kernel, int64_t *steps);
 
 /* Geometry of the last streaming-kernel launch: row strips, work items
  * (strips x warp columns) and CTAs. */

@@ -149,6 +149,8 @@ int warps_per_smsp(StepKernel kern) {
 // is twice the narrow kernel's per stage, so K = 16 spills: K = 14 (bare loop,
 // 252 registers) and K = 12 (all metric modes). The run's tail blocks (fewer
 // steps left than K) use the narrow kernel.
+constexpr int kEoDepth = 14;     // steps per even/odd-layout launch
+constexpr int kEoMinSteps = 56;  // shorter runs skip the layout conversion
 StepKernel pick_wide(int k, int count, bool tma = true) {
     if (k == 14 && count == 0) return tma ? step_wide_kernel<14, 0, true> : step_wide_kernel<14, 0, false>;
     if (k == 12) return count == 2 ? step_wide_kernel<12, 2> : count ? step_wide_kernel<12, 1> : step_wide_kernel<12, 0>;
@@ -201,14 +203,18 @@ struct bml_dev {
     int device = 0;
     uint32_t last_mask = kFull;
     int mode = kGeneric;
-    int variant = 0;  // streaming kernel: 0 auto, 1 narrow (32 cells/lane), 2 / 3 wide (64 cells/lane), K 14 / 12
+    int variant = 0;  // streaming kernel: 0 auto, 1 narrow (32 cells/lane), 2 / 3 wide (64 cells/lane), K 14 / 12,
+                      // 4 wide LDGSTS, 5 stage-split, 6 wide even/odd layout (bare loop, single band)
+    bool eo_active = false;  // inside run_segment: the buffer is in the even/odd layout
     int block_steps = 16;
     int strip_rows = 0;      // 0 = auto (choose_nstrips); < 0: exactly -strip_rows strips
     int resident = 1;        // 1: use the cluster-resident kernel when the lattice qualifies
     int resident_cluster = 0;  // cluster size actually used by the last resident launch
     int last_nstrips = 0, last_grid = 0, last_items = 0;  // last streaming launch
+    long long kernel_steps[6] = {};  // steps per BML_KERNEL_* in the last bml_dev_step call
     int ns_cache_k[kHalo + 1] = {};        // memoised choose_nstrips per block depth
     int ns_cache_setting[kHalo + 1] = {};  // the strip_rows setting it was computed for
+    bool ns_cache_eo[kHalo + 1] = {};      // ... and whether for the even/odd kernel
     int sms = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
@@ -253,9 +259,21 @@ struct bml_dev {
     // steps per wide launch for a metrics mode (0 = bare loop)
     int wide_depth(int metrics) const { return metrics == 0 && variant != 3 ? 14 : 12; }
     bool wide_auto() const { return false; }
+    // the even/odd-layout wide kernel (bare-loop runs of a single band; the
+    // buffer is converted in place around the run, see run_segment)
+    bool use_eo() const {
+        return wide_ok() && single_band() && (variant == 6 || (variant == 0 && eo_auto()));
+    }
+    // measured faster from n = 32768 (W = 1024 words) on: +4.5% there, +8% at
+    // n = 65536; slower at n <= 16384, where the 60-word windows leave too few
+    // items per SM (profiles/r2_sweep_eo.jsonl)
+    bool eo_auto() const { return W >= 1024; }
+    int eo_depth() const { return kEoDepth; }
     // the stage-split kernel (a warp pair per item): aligned rows; variant 5
     bool use_split() const { return variant == 5 && mode == kAligned; }
-    int ncols() const { return use_wide() ? (W + kWideOut - 1) / kWideOut : narrow_ncols(); }
+    int ncols() const {
+        return eo_active ? (W + kEoOut - 1) / kEoOut : use_wide() ? (W + kWideOut - 1) / kWideOut : narrow_ncols();
+    }
     int narrow_ncols() const {
         if (mode == kFullRow) return 1;
         const int out = mode == kSeam ? kSeamOutWords : kOutWords;
@@ -346,7 +364,7 @@ int create_common(int n, int row_begin, int row_end, int device, bml_dev** out) 
     // start with, so row bands built inside DeviceLattice get it before connecting
     if (const char* v = std::getenv("BML_VARIANT")) {
         const int iv = std::atoi(v);
-        if (iv >= 0 && iv <= 5) d->variant = iv;
+        if (iv >= 0 && iv <= 6) d->variant = iv;
     }
     cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, device);
 
@@ -450,9 +468,15 @@ int choose_nstrips(const bml_dev* d, int k, int warps_per_sm, int ncols) {
 
 int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int metrics_stride) {
     const int metrics = count ? (census ? 2 : 1) : 0;
-    const bool wide = d->use_wide() && pick_wide(k, metrics);
+    const bool eo = d->eo_active && k == d->eo_depth() && metrics == 0;
+    if (d->eo_active && !eo) return fail(BML_EINVAL, "even/odd layout: bare-loop launches of 14 steps only");
+    const bool wide = eo || (d->use_wide() && pick_wide(k, metrics));
     const bool split = !wide && d->use_split() && pick_split(k, d->mode, metrics);
-    StepKernel kern = wide ? pick_wide(k, metrics, d->variant != 4)
+    // even/odd layout: K = 14, the TB phase of the even word in departures form
+    // (TBD = 1). Measured against TBD = 0 / 2, K = 16 (TBD = 2, 248 registers) and
+    // three warps per SMSP at K = 8 / 10: profiles/r2_sweep_eo.jsonl
+    StepKernel kern = eo ? step_wide_kernel<kEoDepth, 0, false, 256, true, 1>
+                      : wide ? pick_wide(k, metrics, d->variant != 4)
                       : split ? pick_split(k, d->mode, metrics)
                               : pick(k, d->mode, metrics);
     if (!kern) return fail(BML_EINVAL, "unsupported block depth " + std::to_string(k));
@@ -460,7 +484,7 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
     // every strip has >= min(strip_rows, 16) rows, so for connected bands the
     // ghost-row sources of a band never straddle strips
     // the model scans every strip count: memoised per (k, strip setting)
-    if (d->ns_cache_k[k] <= 0 || d->ns_cache_setting[k] != d->strip_rows) {
+    if (d->ns_cache_k[k] <= 0 || d->ns_cache_setting[k] != d->strip_rows || d->ns_cache_eo[k] != eo) {
         if (split && d->strip_rows == 0) {
             // one item per warp pair, kSplitMaxThreads / 64 pairs per SM
             const int cols = d->narrow_ncols();
@@ -468,10 +492,11 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
             const int max_strips = std::max(1, d->rows / (d->connected ? kHalo : 1));
             d->ns_cache_k[k] = std::max(1, std::min(max_strips, want / cols));  // one round: items <= want
         } else {
-            d->ns_cache_k[k] = choose_nstrips(d, k, 4 * (wide ? std::min(2, u_max) : u_max),
+            d->ns_cache_k[k] = choose_nstrips(d, k, 4 * (wide && !eo ? std::min(2, u_max) : u_max),
                                               wide ? d->ncols() : d->narrow_ncols());
         }
         d->ns_cache_setting[k] = d->strip_rows;
+        d->ns_cache_eo[k] = eo;
     }
     int nstrips = d->ns_cache_k[k];
     // metrics kernels pack two per-lane counters into 16-bit halves: a strip
@@ -519,7 +544,7 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
     }
 
     // one CTA per SM with 4u warps, u = the warps per SMSP the items need
-    const int u = std::min(wide ? 2 : u_max, std::max(1, (a.items + 4 * d->sms - 1) / (4 * d->sms)));
+    const int u = std::min(wide && !eo ? 2 : u_max, std::max(1, (a.items + 4 * d->sms - 1) / (4 * d->sms)));
     const int grid = std::max(1, std::min(d->sms, a.items));
     // split: threads = 64 per warp pair, one pair per item per CTA round
     const int threads = split ? 64 * std::min(kSplitMaxThreads / 64, std::max(1, (a.items + d->sms - 1) / d->sms))
@@ -528,6 +553,7 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
         if (StepKernel narrow = pick_narrow(k, d->mode, metrics)) kern = narrow;
     }
     d->last_nstrips = nstrips;
+    d->kernel_steps[eo ? BML_KERNEL_WIDE_EO : wide ? BML_KERNEL_WIDE : split ? BML_KERNEL_SPLIT : BML_KERNEL_NARROW] += k;
     d->last_grid = grid;
     d->last_items = a.items;
 
@@ -744,6 +770,7 @@ int launch_resident(bml_dev* d, long long steps, bool count, long long metrics_b
         ++d->launches;
         d->cur ^= 1;
         d->resident_cluster = cluster;
+        d->kernel_steps[BML_KERNEL_RESIDENT] += steps;
         *used = true;
         return BML_OK;
     }
@@ -855,7 +882,7 @@ int bml_dev_set_resident(bml_dev* d, int mode) {
 
 int bml_dev_set_variant(bml_dev* d, int variant) {
     if (int rc = check(d)) return rc;
-    if (variant < 0 || variant > 5) return fail(BML_EINVAL, "bml_dev_set_variant: 0 (auto) .. 5");
+    if (variant < 0 || variant > 6) return fail(BML_EINVAL, "bml_dev_set_variant: 0 (auto) .. 6");
     if (d->connected)
         return fail(BML_EINVAL, "bml_dev_set_variant: set before bml_dev_connect (all bands alike)");
     d->variant = variant;
@@ -866,6 +893,16 @@ int bml_dev_set_variant(bml_dev* d, int variant) {
 int bml_dev_path(bml_dev* d, int* resident_cluster) {
     if (!d) return fail(BML_EINVAL, "null bml_dev handle");
     if (resident_cluster) *resident_cluster = d->resident_cluster;
+    return BML_OK;
+}
+
+int bml_dev_last_kernel(bml_dev* d, int* kernel, int64_t* steps) {
+    if (!d) return fail(BML_EINVAL, "null bml_dev handle");
+    int best = BML_KERNEL_NONE;
+    for (int k = 1; k < 6; ++k)
+        if (d->kernel_steps[k] > d->kernel_steps[best]) best = k;
+    if (kernel) *kernel = best;
+    if (steps) *steps = d->kernel_steps[best];
     return BML_OK;
 }
 
@@ -1130,8 +1167,30 @@ int run_segment(bml_dev* d, long long from, long long seg, bool count, bool ever
         return BML_OK;
     }
     const int metrics = count ? (every ? 2 : 1) : 0;
+    long long done = 0;
+    if (!count && d->use_eo() && d->block_steps == 16 && seg >= kEoMinSteps) {
+        // even/odd layout for the whole 14-step blocks of the run: convert the
+        // current buffer (ghost rows included) in place, step, convert back
+        const long long rows_total = d->rows + 2 * kHalo;
+        const int pairs = d->W / 2;
+        const long long threads = rows_total * pairs;
+        const unsigned blocks = static_cast<unsigned>((threads + 255) / 256);
+        eo_convert_kernel<true><<<blocks, 256, 0, d->stream>>>(d->buf[d->cur], rows_total, d->pitch, pairs);
+        BML_CUDA(cudaGetLastError());
+        d->eo_active = true;
+        const int ek = d->eo_depth();
+        for (; seg - done >= ek; done += ek) {
+            if (int rc = launch_block(d, ek, false, false, static_cast<int>(from + done), stride)) {
+                d->eo_active = false;
+                return rc;
+            }
+        }
+        d->eo_active = false;
+        eo_convert_kernel<false><<<blocks, 256, 0, d->stream>>>(d->buf[d->cur], rows_total, d->pitch, pairs);
+        BML_CUDA(cudaGetLastError());
+    }
     const int wk = d->use_wide() && d->block_steps == 16 ? d->wide_depth(metrics) : 0;
-    for (long long done = 0; done < seg;) {
+    for (; done < seg;) {
         const int k = (wk && seg - done >= wk) ? wk : largest_block_at_most(seg - done, d->block_steps);
         if (int rc = launch_block(d, k, count, every, static_cast<int>(from + done), stride)) return rc;
         if (count) {
@@ -1180,6 +1239,7 @@ int bml_dev_step(bml_dev* d, int64_t steps, int64_t* lr_moved, int64_t* tb_moved
     }
     std::vector<char> measured(count ? static_cast<size_t>(steps) : 0, 0);
     d->resident_cluster = 0;
+    std::fill(std::begin(d->kernel_steps), std::end(d->kernel_steps), 0LL);
     const int stride = static_cast<int>(steps);
     long long done = 0;
     size_t fi = 0;

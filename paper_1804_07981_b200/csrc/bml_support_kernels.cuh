@@ -202,6 +202,53 @@ __global__ void counts_kernel(const uint2* __restrict__ buf, int W, int pitch, i
 }
 
 
+// ------------------------------------------------------------ even/odd layout
+// The wide kernel's EO mode (bml_wide_kernel.cuh) keeps each 64-cell group
+// (words 2g, 2g+1) as its even cells, then its odd cells. These convert a
+// whole buffer (every row including the ghost rows) in place, one thread per
+// word pair, both planes; 16-byte accesses, HBM-bound (one read + one write).
+__device__ __forceinline__ uint32_t even_bits(uint32_t x) {  // bits 0,2,..,30 -> 0..15
+    x &= 0x55555555u;
+    x = (x | (x >> 1)) & 0x33333333u;
+    x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+    x = (x | (x >> 4)) & 0x00FF00FFu;
+    return (x | (x >> 8)) & 0x0000FFFFu;
+}
+__device__ __forceinline__ uint32_t spread_bits(uint32_t x) {  // bits 0..15 -> 0,2,..,30
+    x &= 0x0000FFFFu;
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    return (x | (x << 1)) & 0x55555555u;
+}
+// (a, b) = cells 0..31, 32..63 of a group  <->  (e, o) = its even, odd cells
+__device__ __forceinline__ void to_eo(uint32_t a, uint32_t b, uint32_t& e, uint32_t& o) {
+    e = even_bits(a) | (even_bits(b) << 16);
+    o = even_bits(a >> 1) | (even_bits(b >> 1) << 16);
+}
+__device__ __forceinline__ void from_eo(uint32_t e, uint32_t o, uint32_t& a, uint32_t& b) {
+    a = spread_bits(e) | (spread_bits(o) << 1);
+    b = spread_bits(e >> 16) | (spread_bits(o >> 16) << 1);
+}
+template <bool TO_EO>
+__global__ void eo_convert_kernel(uint2* base, long long rows_total, int pitch, int pairs) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= rows_total * pairs) return;
+    const long long r = idx / pairs;
+    const int p = static_cast<int>(idx - r * pairs);
+    uint4* q = reinterpret_cast<uint4*>(base + r * pitch + 2 * p);
+    const uint4 v = *q;  // {L0, T0, L1, T1}
+    uint4 w;
+    if (TO_EO) {
+        to_eo(v.x, v.z, w.x, w.z);
+        to_eo(v.y, v.w, w.y, w.w);
+    } else {
+        from_eo(v.x, v.z, w.x, w.z);
+        from_eo(v.y, v.w, w.y, w.w);
+    }
+    *q = w;
+}
+
 // TEST HOOK (bml_dev_debug_fault): toggle one cell, Empty <-> LR, TB -> Empty.
 __global__ void debug_toggle_kernel(uint2* row0, int pitch, int row, int col) {
     if (threadIdx.x != 0) return;

@@ -29,6 +29,7 @@ namespace bml_k {
 // per-warp ring of kWideRing slots, each completed on its own mbarrier; the
 // lanes wait on the slot's barrier and read their 16-byte pair with one LDS.
 constexpr int kWideOut = 62;   // output words per warp window
+constexpr int kEoOut = 60;     // even/odd layout: output words per window (lanes 1..30)
 constexpr int kWideRing = 6;   // == the loop unroll factor (slot index compile-time)
 constexpr int kWideSlotWords = 64;
 
@@ -102,7 +103,20 @@ __device__ __forceinline__ void wide_store(const StepArgs& a, WideCtx& c, int o,
     c.outp += a.pitch;
 }
 
-template <int K, int COUNT, int P>
+// EO (even/odd layout, see eo_convert_kernel): a lane's two words are the EVEN
+// and the ODD cells of its 64-cell group (bit b of word 0 is cell 64g + 2b, of
+// word 1 cell 64g + 2b + 1). An odd cell's left neighbour and an even cell's
+// right neighbour are then the same bit of the lane's other word, so the LR
+// phase needs 2 funnel shifts per 64 cells instead of 4 (5 ALU-pipe
+// instructions per 32 cells and step instead of 6):
+//   even cell 2b:   left 2b-1 = odd bit b-1 (bit 31 of the left lane's odd word for b = 0),
+//                   right 2b+1 = odd bit b
+//   odd cell 2b+1:  left 2b = even bit b,
+//                   right 2b+2 = even bit b+1 (bit 0 of the right lane's even word for b = 31)
+// TBD: the first TBD words of the pair run the TB phase in departures form,
+// D = T & ~Op(below), newT = T - D + D(above) (1 LOP3 + 2 IMAD instead of 2 LOP3:
+// moves ALU-pipe work to the FMA pipe); their oc slot carries D(above).
+template <int K, int COUNT, int P, bool EO = false, int TBD = 0>
 __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const int j, const StepArgs& a,
                                           WideCtx& c) {
     constexpr int P3 = P % 3, P2 = P % 2;
@@ -122,20 +136,25 @@ __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const 
         // ---- LR phase on row j - 2s (cells: bit b of word w is cell 32w + b)
         const uint32_t O0 = BML_IMAD_OR ? imad(L[0], a.one, T[0]) : (L[0] | T[0]);
         const uint32_t O1 = BML_IMAD_OR ? imad(L[1], a.one, T[1]) : (L[1] | T[1]);
-        const uint32_t Ll = __shfl_up_sync(kFull, L[1], 1);    // left lane's high word
-        const uint32_t Or = __shfl_down_sync(kFull, O0, 1);    // right lane's low word
-        const uint32_t prevL0 = __funnelshift_l(Ll, L[0], 1);
-        const uint32_t prevL1 = __funnelshift_l(L[0], L[1], 1);
-        const uint32_t nextO0 = __funnelshift_r(O0, O1, 1);
-        const uint32_t nextO1 = __funnelshift_r(O1, Or, 1);
-        uint32_t Lp[2], Op[2], newT[2];
+        const uint32_t Ll = __shfl_up_sync(kFull, L[1], 1);    // left lane's high (odd) word
+        const uint32_t Or = __shfl_down_sync(kFull, O0, 1);    // right lane's low (even) word
+        const uint32_t prevL0 = __funnelshift_l(Ll, EO ? L[1] : L[0], 1);
+        const uint32_t prevL1 = EO ? L[0] : __funnelshift_l(L[0], L[1], 1);
+        const uint32_t nextO0 = EO ? O1 : __funnelshift_r(O0, O1, 1);
+        const uint32_t nextO1 = __funnelshift_r(EO ? O0 : O1, Or, 1);
+        uint32_t Lp[2], Op[2], newT[2], D[2];
         Lp[0] = (prevL0 & ~O0) | (L[0] & nextO0);
         Lp[1] = (prevL1 & ~O1) | (L[1] & nextO1);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             Op[h] = BML_IMAD_OR ? imad(Lp[h], a.one, T[h]) : (Lp[h] | T[h]);
             // ---- TB phase emits row j - 2s - 1
-            newT[h] = (tA[h] & ~q.oc[s][h]) | (tB[h] & Op[h]);
+            if (h < TBD) {
+                D[h] = tB[h] & ~Op[h];
+                newT[h] = imad(q.oc[s][h], a.one, imad(D[h], 0u - a.one, tB[h]));
+            } else {
+                newT[h] = (tA[h] & ~q.oc[s][h]) | (tB[h] & Op[h]);
+            }
         }
         if (COUNT) {
             const int rho = j - 2 * s;
@@ -164,7 +183,7 @@ __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const 
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            q.oc[s][h] = Op[h];
+            q.oc[s][h] = h < TBD ? D[h] : Op[h];
             q.lp[s][P2][h] = Lp[h];
             if (s < K - 1) q.nt[s][P3][h] = newT[h];
         }
@@ -196,8 +215,9 @@ __device__ __noinline__ void wide_copy_images(const StepArgs& a, int r_lo, int r
 
 // TMA: rows by bulk copies into the mbarrier ring (true), or by per-lane 16-byte
 // cp.async (LDGSTS) into a commit-group ring like step_block_kernel's (false).
-template <int K, int COUNT, bool TMA = true, int MAXT = 256>
+template <int K, int COUNT, bool TMA = true, int MAXT = 256, bool EO = false, int TBD = 0>
 __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
+    static_assert(!(EO && TMA), "the even/odd layout uses the LDGSTS ring");
     if (BML_PDL) {
         asm volatile("griddepcontrol.launch_dependents;");
         asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous launch's rows are final
@@ -234,16 +254,19 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
         c.lane = lane;
         c.r_lo = static_cast<int>(static_cast<long long>(strip) * a.rows / a.nstrips);
         c.r_hi = static_cast<int>(static_cast<long long>(strip + 1) * a.rows / a.nstrips);
-        const int win = kWideOut * col - 2;            // window start (may be -2)
+        const int win = (EO ? kEoOut : kWideOut) * col - 2;  // window start (may be -2)
         const int g0 = win + 2 * lane;                 // this lane's first word, unwrapped
-        // outputs: window words 1..62, unwrapped index in [-1, W-2]
-        const bool o0 = lane > 0 && g0 <= a.W - 2;
-        const bool o1 = lane < 31 && g0 + 1 <= a.W - 2;
+        // outputs: window words 1..62, unwrapped index in [-1, W-2]; EO: whole
+        // 64-cell groups, lanes 1..30 (words 2..61, unwrapped index in [0, W-1])
+        const bool o0 = EO ? (lane > 0 && lane < 31 && g0 <= a.W - 2) : (lane > 0 && g0 <= a.W - 2);
+        const bool o1 = EO ? o0 : (lane < 31 && g0 + 1 <= a.W - 2);
         c.v0 = o0 ? kFull : 0u;
         c.v1 = o1 ? kFull : 0u;
         c.span = (o0 || o1) ? static_cast<unsigned>(c.r_hi - c.r_lo) : 0u;
         c.kind = (o0 ? 1 : 0) | (o1 ? 2 : 0);
-        const int w0 = g0 < 0 ? g0 + a.W : g0;         // wrapped first word (even)
+        // wrapped first word (even). EO: fully mod W, since the ghost group right
+        // of the last output group must hold the row's first cells
+        const int w0 = EO ? (g0 < 0 ? g0 + a.W : (g0 >= a.W ? g0 - a.W : g0)) : (g0 < 0 ? g0 + a.W : g0);
 
         if (!a.single_band) {
             if (c.r_lo == 0) wait_flag(a.top_flag, a.expect, a.error_flag);
@@ -317,12 +340,12 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
         using P4 = std::integral_constant<int, 4>;
         using P5 = std::integral_constant<int, 5>;
         for (int j = j_begin; j < j_end; j += 6) {
-            wide_iter<K, COUNT, 0>(q, next_row(P0{}), j, a, c);
-            wide_iter<K, COUNT, 1>(q, next_row(P1{}), j + 1, a, c);
-            wide_iter<K, COUNT, 2>(q, next_row(P2{}), j + 2, a, c);
-            wide_iter<K, COUNT, 3>(q, next_row(P3{}), j + 3, a, c);
-            wide_iter<K, COUNT, 4>(q, next_row(P4{}), j + 4, a, c);
-            wide_iter<K, COUNT, 5>(q, next_row(P5{}), j + 5, a, c);
+            wide_iter<K, COUNT, 0, EO, TBD>(q, next_row(P0{}), j, a, c);
+            wide_iter<K, COUNT, 1, EO, TBD>(q, next_row(P1{}), j + 1, a, c);
+            wide_iter<K, COUNT, 2, EO, TBD>(q, next_row(P2{}), j + 2, a, c);
+            wide_iter<K, COUNT, 3, EO, TBD>(q, next_row(P3{}), j + 3, a, c);
+            wide_iter<K, COUNT, 4, EO, TBD>(q, next_row(P4{}), j + 4, a, c);
+            wide_iter<K, COUNT, 5, EO, TBD>(q, next_row(P5{}), j + 5, a, c);
         }
         // the last kWideRing - 1 issues (rows j_end .. j_end + 4) were never
         // consumed: wait for them so every slot's parity is in step for the next item
