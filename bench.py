@@ -702,6 +702,7 @@ def run_b200_multi(args, wl):
         dist.barrier()
         wall = time.perf_counter() - t0
     timed_launches, _ = band.kernel_stats(reset=True)
+    band_kernel = KERNEL_NAMES.get(band.last_kernel(), "step_block_kernel")
     # roofline pass, outside the timed region: per-launch CUDA events
     band.enable_timing(True)
     dist.barrier()
@@ -753,7 +754,7 @@ def run_b200_multi(args, wl):
             "data": "synthetic: reference init_grid(n, rho, seed) lattice",
             "config": dict(config_block(args, desc, n, rho, seed, steps, world), shared_gpu=shared_gpu),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "step_block_kernel",
+                         "frac": achieved / peak, "traffic": None, "kernel": band_kernel,
                          "peak_source": peak_src, "launches_per_rank": launches,
                          "frac_datasheet": achieved / DATASHEET_HBM_GBS,  # per rank, like frac
                          "binding_bound": "alu (per rank; see the N=1 line's roofline_alu)",
@@ -761,7 +762,10 @@ def run_b200_multi(args, wl):
             "cpu_baseline": None,
             "e2e": {"value": n * n * steps * args.steps / float(et[0]) / 1e9, "unit": "Gcell-updates/s",
                     "h2d_bytes_per_step": n * n, "d2h_bytes_per_step": n * n},
-            "gpu_launches": timed_launches * world, "wall_s": wall, "clocks": clocks.summary(),
+            # step kernels + the even/odd layout's 4 conversion kernels (own rows and
+            # ghost rows, in and out) per rank and bml_dev_step call when it ran
+            "gpu_launches": (timed_launches + (4 * args.steps if "even/odd" in band_kernel else 0)) * world,
+            "wall_s": wall, "clocks": clocks.summary(),
             "parity": {"digest": f"0x{digest:016x}", "vehicles": list(k_total), "conserved": conserved,
                        "steps": steps, "golden": golden["file"] if golden else None,
                        "expected_final": golden["final_digest"] if golden and golden["steps"] == steps

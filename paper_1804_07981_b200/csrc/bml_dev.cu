@@ -261,8 +261,10 @@ struct bml_dev {
     bool wide_auto() const { return false; }
     // the even/odd-layout wide kernel (bare-loop runs of a single band; the
     // buffer is converted in place around the run, see run_segment)
+    // single bands, and connected row bands (all bands of a lattice take the same
+    // decision: same n, variant and call sequence)
     bool use_eo() const {
-        return wide_ok() && single_band() && (variant == 6 || (variant == 0 && eo_auto()));
+        return wide_ok() && (single_band() || connected) && (variant == 6 || (variant == 0 && eo_auto()));
     }
     // measured faster from n = 32768 (W = 1024 words) on: +4.5% there, +8% at
     // n = 65536; slower at n <= 16384, where the 60-word windows leave too few
@@ -1155,6 +1157,33 @@ int bml_dev_debug_fault(bml_dev* d, int64_t at_step, int row, int col) {
 
 namespace {
 
+// In-place layout conversion of the current buffer (to or from the even/odd
+// layout). A single band converts its rows and ghost rows in one pass; a
+// connected band converts its own rows, then its ghost rows once both
+// neighbours have published every launch so far (their last launch wrote them).
+int eo_convert(bml_dev* d, bool to_eo) {
+    const int pairs = d->W / 2;
+    const long long rows_total = d->connected ? d->rows : d->rows + 2 * kHalo;
+    uint2* base = d->connected ? d->row0(d->cur) : d->buf[d->cur];
+    const unsigned blocks = static_cast<unsigned>((rows_total * pairs + 255) / 256);
+    if (to_eo)
+        eo_convert_kernel<true><<<blocks, 256, 0, d->stream>>>(base, rows_total, d->pitch, pairs);
+    else
+        eo_convert_kernel<false><<<blocks, 256, 0, d->stream>>>(base, rows_total, d->pitch, pairs);
+    BML_CUDA(cudaGetLastError());
+    if (d->connected) {
+        const dim3 g(static_cast<unsigned>((kHalo * pairs + 255) / 256), 2);
+        if (to_eo)
+            eo_convert_ghost_kernel<true><<<g, 256, 0, d->stream>>>(d->row0(d->cur), d->pitch, pairs, d->rows,
+                                                                    d->flags, d->flags + 1, d->pub_sum, d->err + 1);
+        else
+            eo_convert_ghost_kernel<false><<<g, 256, 0, d->stream>>>(d->row0(d->cur), d->pitch, pairs, d->rows,
+                                                                     d->flags, d->flags + 1, d->pub_sum, d->err + 1);
+        BML_CUDA(cudaGetLastError());
+    }
+    return BML_OK;
+}
+
 // `seg` steps from step `from` of the current call: the resident kernel when the
 // lattice qualifies, else streaming launches of <= block_steps steps. `measured`
 // marks the steps whose census the kernels took.
@@ -1171,12 +1200,7 @@ int run_segment(bml_dev* d, long long from, long long seg, bool count, bool ever
     if (!count && d->use_eo() && d->block_steps == 16 && seg >= kEoMinSteps) {
         // even/odd layout for the whole 14-step blocks of the run: convert the
         // current buffer (ghost rows included) in place, step, convert back
-        const long long rows_total = d->rows + 2 * kHalo;
-        const int pairs = d->W / 2;
-        const long long threads = rows_total * pairs;
-        const unsigned blocks = static_cast<unsigned>((threads + 255) / 256);
-        eo_convert_kernel<true><<<blocks, 256, 0, d->stream>>>(d->buf[d->cur], rows_total, d->pitch, pairs);
-        BML_CUDA(cudaGetLastError());
+        if (int rc = eo_convert(d, true)) return rc;
         d->eo_active = true;
         const int ek = d->eo_depth();
         for (; seg - done >= ek; done += ek) {
@@ -1186,8 +1210,7 @@ int run_segment(bml_dev* d, long long from, long long seg, bool count, bool ever
             }
         }
         d->eo_active = false;
-        eo_convert_kernel<false><<<blocks, 256, 0, d->stream>>>(d->buf[d->cur], rows_total, d->pitch, pairs);
-        BML_CUDA(cudaGetLastError());
+        if (int rc = eo_convert(d, false)) return rc;
     }
     const int wk = d->use_wide() && d->block_steps == 16 ? d->wide_depth(metrics) : 0;
     for (; done < seg;) {

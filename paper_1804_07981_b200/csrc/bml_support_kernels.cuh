@@ -231,13 +231,8 @@ __device__ __forceinline__ void from_eo(uint32_t e, uint32_t o, uint32_t& a, uin
     b = spread_bits(e >> 16) | (spread_bits(o >> 16) << 1);
 }
 template <bool TO_EO>
-__global__ void eo_convert_kernel(uint2* base, long long rows_total, int pitch, int pairs) {
-    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= rows_total * pairs) return;
-    const long long r = idx / pairs;
-    const int p = static_cast<int>(idx - r * pairs);
-    uint4* q = reinterpret_cast<uint4*>(base + r * pitch + 2 * p);
-    const uint4 v = *q;  // {L0, T0, L1, T1}
+__device__ __forceinline__ void eo_convert_pair(uint4* q) {
+    const uint4 v = __ldcg(q);  // {L0, T0, L1, T1}
     uint4 w;
     if (TO_EO) {
         to_eo(v.x, v.z, w.x, w.z);
@@ -247,6 +242,31 @@ __global__ void eo_convert_kernel(uint2* base, long long rows_total, int pitch, 
         from_eo(v.y, v.w, w.y, w.w);
     }
     *q = w;
+}
+template <bool TO_EO>
+__global__ void eo_convert_kernel(uint2* base, long long rows_total, int pitch, int pairs) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= rows_total * pairs) return;
+    const long long r = idx / pairs;
+    const int p = static_cast<int>(idx - r * pairs);
+    eo_convert_pair<TO_EO>(reinterpret_cast<uint4*>(base + r * pitch + 2 * p));
+}
+// A connected band's ghost rows are written by its neighbours' kernels: convert
+// them only once the neighbour has published every launch so far (its flag has
+// reached `expect`, the band's running sum, see StepArgs::expect). blockIdx.y = 0:
+// the kHalo rows above the band (from the up neighbour, top flag), 1: below.
+template <bool TO_EO>
+__global__ void eo_convert_ghost_kernel(uint2* row0, int pitch, int pairs, int rows, const unsigned long long* top_flag,
+                                        const unsigned long long* bot_flag, unsigned long long expect, int* err) {
+    const bool below = blockIdx.y != 0;
+    if (threadIdx.x < 32) wait_flag(below ? bot_flag : top_flag, expect, err);
+    __syncthreads();
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long long>(kHalo) * pairs) return;
+    const int r = static_cast<int>(idx / pairs);
+    const int p = static_cast<int>(idx - static_cast<long long>(r) * pairs);
+    const long long row = below ? rows + r : r - kHalo;
+    eo_convert_pair<TO_EO>(reinterpret_cast<uint4*>(row0 + row * pitch + 2 * p));
 }
 
 // TEST HOOK (bml_dev_debug_fault): toggle one cell, Empty <-> LR, TB -> Empty.

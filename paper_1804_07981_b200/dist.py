@@ -70,6 +70,7 @@ class _Abi:
         lib.bml_dev_upload.argtypes = [vp, vp, ctypes.c_size_t]
         lib.bml_dev_download.argtypes = [vp, vp, ctypes.c_size_t]
         lib.bml_dev_step.argtypes = [vp, ctypes.c_int64, vp, vp, vp, vp]
+        lib.bml_dev_last_kernel.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64)]
         lib.bml_dev_counts.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
         lib.bml_dev_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_size_t)]
         lib.bml_dev_connect.argtypes = [vp, vp, vp]
@@ -167,6 +168,12 @@ class BandLattice:
 
     def enable_timing(self, on=True):
         self.abi.check(self.abi.lib.bml_dev_enable_timing(self.h, 1 if on else 0), "timing")
+
+    def last_kernel(self):
+        """BML_KERNEL_* of the step kernel that ran most of the last step() call."""
+        k, st = ctypes.c_int(), ctypes.c_int64()
+        self.abi.check(self.abi.lib.bml_dev_last_kernel(self.h, ctypes.byref(k), ctypes.byref(st)), "last_kernel")
+        return k.value
 
     def kernel_stats(self, reset=False):
         n = ctypes.c_int64()

@@ -22,11 +22,12 @@ def free_port():
         return s.getsockname()[1]
 
 
-def run_bench(nproc, *args, timeout=900):
+def run_bench(nproc, *args, timeout=900, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={free_port()}", "bench.py", "--gpus", str(nproc),
            *args]
-    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout,
+                         env=None if env is None else {**os.environ, **env})
     assert out.returncode == 0, out.stderr[-2000:]
     return json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
 
@@ -45,6 +46,21 @@ def test_two_rank_bench_matches_single_band(gpu):
     assert par["conserved"]
     cfg = line["config"]
     assert cfg["n"] == 1440  # ~2x the cells of N=1024, side a multiple of 32
+    digest, counts = single_band_digest(gpu, cfg["n"], cfg["rho"], cfg["seed"], par["steps"])
+    assert par["digest"] == digest
+    assert counts == par["vehicles"]
+
+
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_even_odd_row_bands_match_single_band(gpu, ranks):
+    """The even/odd-layout kernel on connected row bands (BML_VARIANT=6 forces it at
+    N=8192): each rank converts its rows in place, and its ghost rows once the
+    neighbours' flags say their last launch wrote them; 10000 steps per run."""
+    line = run_bench(ranks, "--workload", "c2ff", "--steps", "1", "--warmup", "1", "--no-cpu",
+                     env={"BML_VARIANT": "6"})
+    cfg = line["config"]
+    assert cfg["n"] == 8192
+    par = line["parity"]
     digest, counts = single_band_digest(gpu, cfg["n"], cfg["rho"], cfg["seed"], par["steps"])
     assert par["digest"] == digest
     assert counts == par["vehicles"]
