@@ -270,7 +270,9 @@ struct bml_dev {
     // n = 65536; slower at n <= 16384, where the 60-word windows leave too few
     // items per SM (profiles/r2_sweep_eo.jsonl)
     bool eo_auto() const { return W >= 1024; }
-    int eo_depth() const { return kEoDepth; }
+    // steps per even/odd launch: 14 (bare loop), 12 (metric modes: the counters
+    // need registers, as in the wide kernel)
+    int eo_depth(int metrics) const { return metrics ? 12 : kEoDepth; }
     // the stage-split kernel (a warp pair per item): aligned rows; variant 5
     bool use_split() const { return variant == 5 && mode == kAligned; }
     int ncols() const {
@@ -470,14 +472,16 @@ int choose_nstrips(const bml_dev* d, int k, int warps_per_sm, int ncols) {
 
 int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int metrics_stride) {
     const int metrics = count ? (census ? 2 : 1) : 0;
-    const bool eo = d->eo_active && k == d->eo_depth() && metrics == 0;
-    if (d->eo_active && !eo) return fail(BML_EINVAL, "even/odd layout: bare-loop launches of 14 steps only");
+    const bool eo = d->eo_active && k == d->eo_depth(metrics);
+    if (d->eo_active && !eo) return fail(BML_EINVAL, "even/odd layout: launches of 14 (12 with metrics) steps only");
     const bool wide = eo || (d->use_wide() && pick_wide(k, metrics));
     const bool split = !wide && d->use_split() && pick_split(k, d->mode, metrics);
     // even/odd layout: K = 14, the TB phase of the even word in departures form
     // (TBD = 1). Measured against TBD = 0 / 2, K = 16 (TBD = 2, 248 registers) and
     // three warps per SMSP at K = 8 / 10: profiles/r2_sweep_eo.jsonl
-    StepKernel kern = eo ? step_wide_kernel<kEoDepth, 0, false, 256, true, 1>
+    StepKernel kern = eo ? (metrics == 2   ? step_wide_kernel<12, 2, false, 256, true, 1>
+                            : metrics == 1 ? step_wide_kernel<12, 1, false, 256, true, 1>
+                                           : step_wide_kernel<kEoDepth, 0, false, 256, true, 1>)
                       : wide ? pick_wide(k, metrics, d->variant != 4)
                       : split ? pick_split(k, d->mode, metrics)
                               : pick(k, d->mode, metrics);
@@ -1197,16 +1201,22 @@ int run_segment(bml_dev* d, long long from, long long seg, bool count, bool ever
     }
     const int metrics = count ? (every ? 2 : 1) : 0;
     long long done = 0;
-    if (!count && d->use_eo() && d->block_steps == 16 && seg >= kEoMinSteps) {
-        // even/odd layout for the whole 14-step blocks of the run: convert the
-        // current buffer (ghost rows included) in place, step, convert back
+    if (d->use_eo() && d->block_steps == 16 && seg >= kEoMinSteps) {
+        // even/odd layout for the whole 14-step (12 with metrics) blocks of the
+        // run: convert the current buffer in place, step, convert back
         if (int rc = eo_convert(d, true)) return rc;
         d->eo_active = true;
-        const int ek = d->eo_depth();
+        const int ek = d->eo_depth(metrics);
         for (; seg - done >= ek; done += ek) {
-            if (int rc = launch_block(d, ek, false, false, static_cast<int>(from + done), stride)) {
+            if (int rc = launch_block(d, ek, count, every, static_cast<int>(from + done), stride)) {
                 d->eo_active = false;
                 return rc;
+            }
+            if (count) {
+                if (every)
+                    std::fill(measured.begin() + from + done, measured.begin() + from + done + ek, 1);
+                else
+                    measured[from + done + ek - 1] = 1;
             }
         }
         d->eo_active = false;

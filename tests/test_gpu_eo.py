@@ -82,13 +82,17 @@ def test_eo_short_runs_and_repeated_calls(gpu, oracle):
     assert lat.counts() == oracle.counts(n, cells)
 
 
-def test_eo_metrics_calls_use_the_counting_kernels(gpu, oracle):
-    """Metrics calls on a variant-6 handle run the (bit-plane) counting kernels."""
-    n, steps = 2048, 60
+@pytest.mark.parametrize("n,steps", [(2048, 60), (4096, 101)])
+@pytest.mark.parametrize("strict", [False, True])
+def test_eo_metrics_match_oracle(gpu, oracle, n, steps, strict):
+    """Metrics calls run the even/odd kernel's counting instantiations (12 steps per
+    launch; moved counts and the census are popcounts, so the layout does not
+    change them), then a narrow tail."""
     cells = oracle.init_grid(n, 0.4, 5)
     _, (lm, tm, lc, tc) = oracle.run(n, cells, steps, metrics=True)
     lat = gpu.DeviceLattice(n)
     set_variant(gpu, lat, 6)
+    lat.set_census(strict)
     lat.upload(gpu.Grid.from_bytes(n, cells))
     ms = lat.step_with_metrics(steps)
     assert [m.lr_moved for m in ms] == lm and [m.tb_moved for m in ms] == tm
@@ -144,3 +148,24 @@ def test_automatic_kernel_choice(gpu, n, steps, kernel, kernel_steps):
     lat.init_random(0.35, 1)
     lat.step(steps)
     assert last_kernel(gpu, lat) == (kernel, kernel_steps)
+
+
+@pytest.mark.parametrize("strict,want", [(True, 21), (False, 32)])
+def test_eo_census_reports_the_fault(gpu, strict, want):
+    """A vehicle removed after step 20 of a 150-step metrics call: the call splits at
+    the fault, the remaining 130 steps run the even/odd kernel (12-step launches);
+    strict census reports step 21, the launch-boundary census step 20 + 12."""
+    import re
+
+    n = 2048
+    lat = gpu.DeviceLattice(n)
+    set_variant(gpu, lat, 6)
+    lat.set_census(strict)
+    g = gpu.init_grid(n, 0.3, 4)
+    lat.upload(g)
+    i = g.to_bytes().index(1)
+    lat.debug_fault(20, *divmod(i, n))
+    with pytest.raises(RuntimeError) as ei:
+        lat.step_with_metrics(150)
+    m = re.search(r"conservation violated at step (\d+) of (\d+)", str(ei.value))
+    assert m and int(m.group(1)) == want, str(ei.value)
