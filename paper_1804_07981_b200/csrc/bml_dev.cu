@@ -376,7 +376,7 @@ int create_common(int n, int row_begin, int row_end, int device, bml_dev** out) 
         bml_dev_destroy(d);
         return cuda_fail(err, what);
     };
-    const size_t words = static_cast<size_t>(d->rows + 2 * kHalo) * d->pitch;
+    const size_t words = static_cast<size_t>(d->rows + 2 * kHalo + kLoadPad) * d->pitch;
     for (int p = 0; p < 2; ++p) {
         if ((e = cudaMalloc(&d->buf[p], words * sizeof(uint2))) != cudaSuccess)
             return bail(e, "cudaMalloc(lattice)");

@@ -11,6 +11,9 @@
 namespace bml_k {
 
 constexpr int kHalo = 16;       // ghost rows per side == max steps fused per launch
+// zero rows allocated after the lower ghost rows: the wide kernel's ring reads
+// (don't-care) rows up to rows + 2K + 8 <= rows + 40 without clamping the address
+constexpr int kLoadPad = 32;
 constexpr int kMaxWarpsPerCta = 12;  // step kernel: one CTA per SM, up to 3 warps per SMSP
 constexpr int kOutWords = 30;      // output words per warp in the haloed modes
 constexpr int kSeamOutWords = 28;  // kSeam: output words per warp (two ghost words per side)

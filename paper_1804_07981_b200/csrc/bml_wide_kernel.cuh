@@ -84,10 +84,24 @@ struct WideCtx {
 };
 
 // Final-stage output: one predicated 16-byte store for a full pair, one 8-byte
-// store for a half pair (the lanes next to the ghost words).
+// store for a half pair (the lanes next to the ghost words). The even/odd layout
+// only has whole pairs: the 8-byte forms (and the register moves that build
+// their aligned operand pairs) are left out.
+template <bool EO>
 __device__ __forceinline__ void wide_store(const StepArgs& a, WideCtx& c, int o, const uint32_t l[2],
                                            const uint32_t t[2]) {
     const bool st = static_cast<unsigned>(o - c.r_lo) < c.span;
+    if (EO) {
+        asm volatile(
+            "{\n .reg .pred pf;\n"
+            " setp.ne.u32 pf, %0, 0;\n"
+            " @pf st.global.v4.u32 [%1], {%2, %3, %4, %5};\n"
+            "}" ::"r"(static_cast<uint32_t>(st)),
+            "l"(c.outp), "r"(l[0]), "r"(t[0]), "r"(l[1]), "r"(t[1])
+            : "memory");
+        c.outp += a.pitch;
+        return;
+    }
     const uint32_t full = st && c.kind == 3, lo = st && c.kind == 1, hi = st && c.kind == 2;
     asm volatile(
         "{\n .reg .pred pf, pl, ph;\n"
@@ -173,7 +187,7 @@ __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const 
         }
         if (s == K - 1) {
             const uint32_t* nl = q.lp[s][(P2 + 1) % 2];
-            wide_store(a, c, j - 2 * K + 1, nl, newT);
+            wide_store<EO>(a, c, j - 2 * K + 1, nl, newT);
             if (COUNT == 1) {  // census after the launch's last step: the stored row (branch-free)
                 const bool st = static_cast<unsigned>(j - 2 * K + 1 - c.r_lo) < c.span;
                 const uint32_t add = __popc(nl[0] & c.v0) + __popc(nl[1] & c.v1) +
@@ -306,7 +320,8 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
         // slot is issued and waited on, branch-free), and the data is don't-care
         const uint2* glast = a.src + static_cast<long long>(j_load_end - 1) * a.pitch;
         auto issue_to = [&](int slot) {
-            const uint2* row = j_issue < j_load_end ? gsrc : glast;
+            // EO: rows past the band end read the zero pad rows (kLoadPad), no select
+            const uint2* row = EO ? gsrc : (j_issue < j_load_end ? gsrc : glast);
             if (TMA) {
                 wide_issue_row(lane == 0, bar_base + 8u * slot, ring_base + slot * kSlotBytes, row + wa, bytes1,
                                row, bytes2);
