@@ -109,7 +109,8 @@ def _golden(name):
                                   "ref_n32768_rho0.35_seed1_steps10000.json",
                                   "ref_n23168_rho0.35_seed1_steps10000.json",
                                   "ref_n46336_rho0.35_seed1_steps10000.json",
-                                  "ref_n65536_rho0.35_seed1_steps1000.json"])
+                                  "ref_n65536_rho0.35_seed1_steps1000.json",
+                                  "ref_n65536_rho0.35_seed1_steps10000.json"])
 def test_eo_reference_goldens(gpu, name):
     """Fully on the device (init -> steps -> digest), against the unmodified
     reference; chained goldens also at every checkpoint."""
