@@ -481,7 +481,9 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
     // three warps per SMSP at K = 8 / 10: profiles/r2_sweep_eo.jsonl
     StepKernel kern = eo ? (metrics == 2   ? step_wide_kernel<12, 2, false, 256, true, 1>
                             : metrics == 1 ? step_wide_kernel<12, 1, false, 256, true, 1>
-                                           : step_wide_kernel<kEoDepth, 0, false, 256, true, 1>)
+                                           : d->pitch == 2048 ? step_wide_kernel<kEoDepth, 0, false, 256, true, 1, 2048>
+                                           : d->pitch == 1024 ? step_wide_kernel<kEoDepth, 0, false, 256, true, 1, 1024>
+                                                              : step_wide_kernel<kEoDepth, 0, false, 256, true, 1>)
                       : wide ? pick_wide(k, metrics, d->variant != 4)
                       : split ? pick_split(k, d->mode, metrics)
                               : pick(k, d->mode, metrics);

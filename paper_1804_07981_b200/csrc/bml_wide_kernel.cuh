@@ -89,7 +89,7 @@ struct WideCtx {
 // their aligned operand pairs) are left out.
 template <bool EO>
 __device__ __forceinline__ void wide_store(const StepArgs& a, WideCtx& c, int o, const uint32_t l[2],
-                                           const uint32_t t[2]) {
+                                           const uint32_t t[2], int pitch) {
     const bool st = static_cast<unsigned>(o - c.r_lo) < c.span;
     if (EO) {
         asm volatile(
@@ -99,7 +99,7 @@ __device__ __forceinline__ void wide_store(const StepArgs& a, WideCtx& c, int o,
             "}" ::"r"(static_cast<uint32_t>(st)),
             "l"(c.outp), "r"(l[0]), "r"(t[0]), "r"(l[1]), "r"(t[1])
             : "memory");
-        c.outp += a.pitch;
+        c.outp += pitch;
         return;
     }
     const uint32_t full = st && c.kind == 3, lo = st && c.kind == 1, hi = st && c.kind == 2;
@@ -114,7 +114,7 @@ __device__ __forceinline__ void wide_store(const StepArgs& a, WideCtx& c, int o,
         "}" ::"r"(full),
         "r"(lo), "r"(hi), "l"(c.outp), "r"(l[0]), "r"(t[0]), "r"(l[1]), "r"(t[1])
         : "memory");
-    c.outp += a.pitch;
+    c.outp += pitch;
 }
 
 // EO (even/odd layout, see eo_convert_kernel): a lane's two words are the EVEN
@@ -130,7 +130,7 @@ __device__ __forceinline__ void wide_store(const StepArgs& a, WideCtx& c, int o,
 // TBD: the first TBD words of the pair run the TB phase in departures form,
 // D = T & ~Op(below), newT = T - D + D(above) (1 LOP3 + 2 IMAD instead of 2 LOP3:
 // moves ALU-pipe work to the FMA pipe); their oc slot carries D(above).
-template <int K, int COUNT, int P, bool EO = false, int TBD = 0>
+template <int K, int COUNT, int P, bool EO = false, int TBD = 0, int PITCH = 0>
 __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const int j, const StepArgs& a,
                                           WideCtx& c) {
     constexpr int P3 = P % 3, P2 = P % 2;
@@ -187,7 +187,7 @@ __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const 
         }
         if (s == K - 1) {
             const uint32_t* nl = q.lp[s][(P2 + 1) % 2];
-            wide_store<EO>(a, c, j - 2 * K + 1, nl, newT);
+            wide_store<EO>(a, c, j - 2 * K + 1, nl, newT, PITCH ? PITCH : a.pitch);
             if (COUNT == 1) {  // census after the launch's last step: the stored row (branch-free)
                 const bool st = static_cast<unsigned>(j - 2 * K + 1 - c.r_lo) < c.span;
                 const uint32_t add = __popc(nl[0] & c.v0) + __popc(nl[1] & c.v1) +
@@ -229,7 +229,9 @@ __device__ __noinline__ void wide_copy_images(const StepArgs& a, int r_lo, int r
 
 // TMA: rows by bulk copies into the mbarrier ring (true), or by per-lane 16-byte
 // cp.async (LDGSTS) into a commit-group ring like step_block_kernel's (false).
-template <int K, int COUNT, bool TMA = true, int MAXT = 256, bool EO = false, int TBD = 0>
+// PITCH: the row pitch in words at compile time (0: StepArgs::pitch), so the
+// unrolled loop addresses its six rows with immediate offsets
+template <int K, int COUNT, bool TMA = true, int MAXT = 256, bool EO = false, int TBD = 0, int PITCH = 0>
 __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
     static_assert(!(EO && TMA), "the even/odd layout uses the LDGSTS ring");
     if (BML_PDL) {
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
                 cp_async_commit();
             }
             ++j_issue;
-            gsrc += a.pitch;
+            gsrc += PITCH ? PITCH : a.pitch;
         };
         auto next_row = [&](auto p_const) -> uint4 {
             constexpr int P = decltype(p_const)::value;
@@ -355,12 +357,12 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
         using P4 = std::integral_constant<int, 4>;
         using P5 = std::integral_constant<int, 5>;
         for (int j = j_begin; j < j_end; j += 6) {
-            wide_iter<K, COUNT, 0, EO, TBD>(q, next_row(P0{}), j, a, c);
-            wide_iter<K, COUNT, 1, EO, TBD>(q, next_row(P1{}), j + 1, a, c);
-            wide_iter<K, COUNT, 2, EO, TBD>(q, next_row(P2{}), j + 2, a, c);
-            wide_iter<K, COUNT, 3, EO, TBD>(q, next_row(P3{}), j + 3, a, c);
-            wide_iter<K, COUNT, 4, EO, TBD>(q, next_row(P4{}), j + 4, a, c);
-            wide_iter<K, COUNT, 5, EO, TBD>(q, next_row(P5{}), j + 5, a, c);
+            wide_iter<K, COUNT, 0, EO, TBD, PITCH>(q, next_row(P0{}), j, a, c);
+            wide_iter<K, COUNT, 1, EO, TBD, PITCH>(q, next_row(P1{}), j + 1, a, c);
+            wide_iter<K, COUNT, 2, EO, TBD, PITCH>(q, next_row(P2{}), j + 2, a, c);
+            wide_iter<K, COUNT, 3, EO, TBD, PITCH>(q, next_row(P3{}), j + 3, a, c);
+            wide_iter<K, COUNT, 4, EO, TBD, PITCH>(q, next_row(P4{}), j + 4, a, c);
+            wide_iter<K, COUNT, 5, EO, TBD, PITCH>(q, next_row(P5{}), j + 5, a, c);
         }
         // the last kWideRing - 1 issues (rows j_end .. j_end + 4) were never
         // consumed: wait for them so every slot's parity is in step for the next item
