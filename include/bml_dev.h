@@ -184,8 +184,9 @@ int bml_dev_debug_fault(bml_dev *dev, int64_t at_step, int row, int col);
  * only, else narrow), 4 = wide with a per-lane cp.async row ring, 5 = stage-split
  * (a warp pair per item), 6 = wide in the even/odd layout (each 64-cell group held
  * as its even then its odd cells, 5 instead of 6 ALU instructions per 32 cells and
- * step; the buffer is converted in place around bare-loop runs of >= 56 steps of a
- * single band, n % 64 == 0, n >= 2048; anything else runs the narrow kernel).
+ * step; the buffer is converted in place around runs of >= 56 steps, n % 64 == 0,
+ * n >= 2048, single bands and connected row bands, bare loop or metrics; anything
+ * else runs the narrow kernel). Automatic (0) picks it from n >= 20480 (W >= 640).
  * Row bands: set on every band before connecting. */
 int bml_dev_set_variant(bml_dev *dev, int variant);
 

@@ -266,10 +266,10 @@ struct bml_dev {
     bool use_eo() const {
         return wide_ok() && (single_band() || connected) && (variant == 6 || (variant == 0 && eo_auto()));
     }
-    // measured faster from n = 32768 (W = 1024 words) on: +4.5% there, +8% at
-    // n = 65536; slower at n <= 16384, where the 60-word windows leave too few
-    // items per SM (profiles/r2_sweep_eo.jsonl)
-    bool eo_auto() const { return W >= 1024; }
+    // measured faster from n = 23168 (W = 724 words) on: +3.5% there, +14% at
+    // n = 32768, +18% at n = 65536; equal at 16384 and slower below, where the
+    // 60-word windows leave too few items per SM (profiles/r2_sweep_eo.jsonl)
+    bool eo_auto() const { return W >= 640; }
     // steps per even/odd launch: 14 (bare loop), 12 (metric modes: the counters
     // need registers, as in the wide kernel)
     int eo_depth(int metrics) const { return metrics ? 12 : kEoDepth; }

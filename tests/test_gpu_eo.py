@@ -139,7 +139,8 @@ def last_kernel(gpu, lat):
 
 
 @pytest.mark.parametrize("n,steps,kernel,kernel_steps", [
-    (32768, 60, 3, 56),   # automatic: the even/odd kernel from n = 32768 on (4 tail steps narrow)
+    (32768, 60, 3, 56),   # automatic: the even/odd kernel from W >= 640 words (4 tail steps narrow)
+    (23168, 70, 3, 70),   # the weak sweep's 1-GPU size (W = 724)
     (16384, 60, 1, 60),   # below: the narrow kernel
     (32768, 40, 1, 40),   # shorter than the conversion threshold: narrow
     (1024, 60, 5, 60),    # resident
