@@ -1212,6 +1212,7 @@ int run_segment(bml_dev* d, long long from, long long seg, bool count, bool ever
         for (; seg - done >= ek; done += ek) {
             if (int rc = launch_block(d, ek, count, every, static_cast<int>(from + done), stride)) {
                 d->eo_active = false;
+                eo_convert(d, false);  // leave the buffer in the standard layout
                 return rc;
             }
             if (count) {
