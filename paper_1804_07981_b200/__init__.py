@@ -40,6 +40,7 @@ try:
         step_phase,
         vehicles_per_species,
         verify_backends,
+        verify_device,
         write_ppm,
     )
 except ImportError as exc:  # pragma: no cover - exercised only on broken installs
@@ -74,6 +75,7 @@ __all__ = [
     "step_phase",
     "vehicles_per_species",
     "verify_backends",
+    "verify_device",
     "write_ppm",
     "LIB_DEV",
 ]

@@ -284,6 +284,11 @@ void DeviceLattice::set_resident(int mode) {
     for (bml_dev* h : bands_) ok(bml_dev_set_resident(h, mode), "bml_dev_set_resident");
 }
 
+void DeviceLattice::set_variant(int variant) {
+    if (bands_.size() > 1) throw std::invalid_argument("set_variant: single-band lattices only");
+    ok(bml_dev_set_variant(bands_[0], variant), "bml_dev_set_variant");
+}
+
 int DeviceLattice::resident_cluster() const {
     int c = 0;
     ok(bml_dev_path(bands_[0], &c), "bml_dev_path");

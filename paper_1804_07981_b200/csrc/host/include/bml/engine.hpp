@@ -128,6 +128,8 @@ public:
     // Small-lattice cluster-resident kernel: enabled by default; resident_cluster()
     // reports the cluster size the last step() used (0 = streaming kernel).
     void set_resident(int mode);  // 0 = off, 1 = ghost-zone kernel (default), 2 = p2p kernel
+    // Streaming-kernel variant (bml_dev_set_variant): 0 automatic, 1 narrow, 6 even/odd layout, ...
+    void set_variant(int variant);
     int resident_cluster() const;
     void set_stream(void* cuda_stream);  // single-band only
     void synchronize() const;

@@ -46,32 +46,19 @@ bool conserved_run(DeviceLattice& lat, long steps, const VehicleCounts& initial)
 
 }  // namespace
 
-VerifyReport verify_backends(const SimConfig& cfg) {
-    validate(cfg);
-    const Grid initial = init_grid({cfg.n, cfg.rho, cfg.seed});
-    const VehicleCounts start = count_vehicles(initial);
+namespace {
 
-    VerifyReport report;
-    std::vector<NamedGrid> finals;
-    auto record = [&](const std::string& name, DeviceLattice& lat) {
+const char* const kDevicePaths[] = {"b200", "b200-streaming", "b200-even-odd", "b200-phases", "b200-bands"};
+
+// One device path from `initial`: the final grid and its digest go into the
+// report, a census difference clears report.conserved.
+void run_device_path(const std::string& name, const SimConfig& cfg, const Grid& initial,
+                     const VehicleCounts& start, VerifyReport& report, std::vector<NamedGrid>& finals) {
+    auto record = [&](DeviceLattice& lat) {
         report.digests.push_back(PathDigest{name, lat.digest()});
         finals.push_back(NamedGrid{name, lat.download()});
     };
-
-    {  // default path: resident cluster kernel when the lattice qualifies
-        DeviceLattice lat(cfg.n);
-        lat.upload(initial);
-        if (!conserved_run(lat, cfg.steps, start)) report.conserved = false;
-        record("b200", lat);
-    }
-    {  // streaming temporally blocked kernel only
-        DeviceLattice lat(cfg.n);
-        lat.set_resident(0);
-        lat.upload(initial);
-        if (!conserved_run(lat, cfg.steps, start)) report.conserved = false;
-        record("b200-streaming", lat);
-    }
-    {  // single-phase kernels, one phase per launch (step_phase)
+    if (name == "b200-phases") {  // single-phase kernels, one phase per launch (step_phase)
         DeviceLattice lat(cfg.n);
         lat.upload(initial);
         for (long s = 0; s < cfg.steps; ++s) {
@@ -80,18 +67,57 @@ VerifyReport verify_backends(const SimConfig& cfg) {
             const VehicleCounts c = lat.counts();
             if (c.lr != start.lr || c.tb != start.tb) report.conserved = false;
         }
-        record("b200-phases", lat);
+        record(lat);
+        return;
     }
-    {  // row bands with in-kernel ghost-row exchange (block depth 1 when too small)
+    if (name == "b200-bands") {  // row bands with in-kernel ghost-row exchange (block depth 1 when too small)
         const int bands = verify_bands(cfg.n);
         DeviceLattice lat(cfg.n, bands);
         if (bands == 1) lat.configure(1, 0);
         lat.upload(initial);
         if (!conserved_run(lat, cfg.steps, start)) report.conserved = false;
-        record("b200-bands", lat);
+        record(lat);
+        return;
     }
+    DeviceLattice lat(cfg.n);
+    if (name == "b200-streaming") {  // narrow streaming temporally blocked kernel only
+        lat.set_resident(0);
+        lat.set_variant(1);
+    } else if (name == "b200-even-odd") {  // even/odd-layout streaming kernel
+        lat.set_resident(0);
+        lat.set_variant(6);
+    } else if (name != "b200") {  // default path: resident cluster kernel when the lattice qualifies
+        throw std::invalid_argument("verify_device: unknown path '" + name + "'");
+    }
+    lat.upload(initial);
+    if (!conserved_run(lat, cfg.steps, start)) report.conserved = false;
+    record(lat);
+}
+
+VerifyReport verify_paths(const SimConfig& cfg, const std::vector<std::string>& paths) {
+    validate(cfg);
+    for (const std::string& p : paths)
+        if (std::find(std::begin(kDevicePaths), std::end(kDevicePaths), p) == std::end(kDevicePaths))
+            throw std::invalid_argument("verify_device: unknown path '" + p + "'");
+    const Grid initial = init_grid({cfg.n, cfg.rho, cfg.seed});
+    const VehicleCounts start = count_vehicles(initial);
+    VerifyReport report;
+    std::vector<NamedGrid> finals;
+    for (const std::string& p : paths) run_device_path(p, cfg, initial, start, report, finals);
     report.mismatch = first_mismatch(finals);
     return report;
+}
+
+}  // namespace
+
+// The reference's four slots (verify.cpp:19-42), filled with four device paths.
+VerifyReport verify_backends(const SimConfig& cfg) {
+    return verify_paths(cfg, {"b200", "b200-streaming", "b200-phases", "b200-bands"});
+}
+
+VerifyReport verify_device(const SimConfig& cfg, const std::vector<std::string>& paths) {
+    if (!paths.empty()) return verify_paths(cfg, paths);
+    return verify_paths(cfg, std::vector<std::string>(std::begin(kDevicePaths), std::end(kDevicePaths)));
 }
 
 }  // namespace bml

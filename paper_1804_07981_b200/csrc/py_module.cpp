@@ -188,6 +188,21 @@ PYBIND11_MODULE(_bml, m) {
           py::arg("threads") = 1,
           "Run the four device code paths from one initial grid and compare bit-exactly.");
 
+    m.def("verify_device",
+          [](int n, double rho, long steps, std::uint64_t seed, std::vector<std::string> paths) {
+              bml::SimConfig cfg;
+              cfg.n = n;
+              cfg.rho = rho;
+              cfg.steps = steps;
+              cfg.seed = seed;
+              cfg.backend = bml::Backend::B200;
+              py::gil_scoped_release nogil;
+              return bml::verify_device(cfg, paths);
+          },
+          py::arg("n"), py::arg("rho"), py::arg("steps"), py::arg("seed") = 1,
+          py::arg("paths") = std::vector<std::string>{},
+          "Cross-check every device code path (or the named subset) from one initial grid, bit-exactly.");
+
     m.def("encode_ppm", [](const bml::Grid& g) {
         const auto bytes = bml::encode_ppm(g);
         return py::bytes(reinterpret_cast<const char*>(bytes.data()), bytes.size());
@@ -281,6 +296,7 @@ PYBIND11_MODULE(_bml, m) {
         .def("configure", &bml::DeviceLattice::configure, py::arg("block_steps") = 0,
              py::arg("strip_rows") = 0)
         .def("set_resident", &bml::DeviceLattice::set_resident, py::arg("mode"))
+        .def("set_variant", &bml::DeviceLattice::set_variant, py::arg("variant"))
         .def_property_readonly("resident_cluster", &bml::DeviceLattice::resident_cluster)
         .def("set_stream",
              [](bml::DeviceLattice& d, std::uintptr_t s) { d.set_stream(reinterpret_cast<void*>(s)); },
