@@ -476,14 +476,15 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
     if (d->eo_active && !eo) return fail(BML_EINVAL, "even/odd layout: launches of 14 (12 with metrics) steps only");
     const bool wide = eo || (d->use_wide() && pick_wide(k, metrics));
     const bool split = !wide && d->use_split() && pick_split(k, d->mode, metrics);
-    // even/odd layout: K = 14, the TB phase of the even word in departures form
-    // (TBD = 1). Measured against TBD = 0 / 2, K = 16 (TBD = 2, 248 registers) and
-    // three warps per SMSP at K = 8 / 10: profiles/r2_sweep_eo.jsonl
-    StepKernel kern = eo ? (metrics == 2   ? step_wide_kernel<12, 2, false, 256, true, 1>
-                            : metrics == 1 ? step_wide_kernel<12, 1, false, 256, true, 1>
-                                           : d->pitch == 2048 ? step_wide_kernel<kEoDepth, 0, false, 256, true, 1, 2048>
-                                           : d->pitch == 1024 ? step_wide_kernel<kEoDepth, 0, false, 256, true, 1, 1024>
-                                                              : step_wide_kernel<kEoDepth, 0, false, 256, true, 1>)
+    // even/odd layout: K = 14; TB phase of the even word in departures form with
+    // IMADs (TBD = 1), of the odd word with the departures carried in LOP3s
+    // (DL = 2). Measured against TBD = 0 / 2, DL = 0 / 3, K = 16 and three warps per
+    // SMSP at K = 8 / 10: profiles/r2_sweep_eo.jsonl
+    StepKernel kern = eo ? (metrics == 2   ? step_wide_kernel<12, 2, false, 256, true, 1, 0, 0>
+                            : metrics == 1 ? step_wide_kernel<12, 1, false, 256, true, 1, 0, 2>
+                                           : d->pitch == 2048 ? step_wide_kernel<kEoDepth, 0, false, 256, true, 1, 2048, 2>
+                                           : d->pitch == 1024 ? step_wide_kernel<kEoDepth, 0, false, 256, true, 1, 1024, 2>
+                                                              : step_wide_kernel<kEoDepth, 0, false, 256, true, 1, 0, 2>)
                       : wide ? pick_wide(k, metrics, d->variant != 4)
                       : split ? pick_split(k, d->mode, metrics)
                               : pick(k, d->mode, metrics);

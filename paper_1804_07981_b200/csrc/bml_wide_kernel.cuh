@@ -130,7 +130,10 @@ __device__ __forceinline__ void wide_store(const StepArgs& a, WideCtx& c, int o,
 // TBD: the first TBD words of the pair run the TB phase in departures form,
 // D = T & ~Op(below), newT = T - D + D(above) (1 LOP3 + 2 IMAD instead of 2 LOP3:
 // moves ALU-pipe work to the FMA pipe); their oc slot carries D(above).
-template <int K, int COUNT, int P, bool EO = false, int TBD = 0, int PITCH = 0>
+// DL (bit h): word h (if not TBD) carries the departures too but combines them
+// with LOP3s, newT = (T & Op(below)) | D(above): the same 2 LOP3 as the plain
+// form, without the T(i-1) register (tA) per stage.
+template <int K, int COUNT, int P, bool EO = false, int TBD = 0, int PITCH = 0, int DL = 0>
 __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const int j, const StepArgs& a,
                                           WideCtx& c) {
     constexpr int P3 = P % 3, P2 = P % 2;
@@ -166,6 +169,9 @@ __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const 
             if (h < TBD) {
                 D[h] = tB[h] & ~Op[h];
                 newT[h] = imad(q.oc[s][h], a.one, imad(D[h], 0u - a.one, tB[h]));
+            } else if (DL & (1 << h)) {  // departures carried, plain LOP3s: no T(i-1) slot
+                D[h] = tB[h] & ~Op[h];
+                newT[h] = (tB[h] & Op[h]) | q.oc[s][h];
             } else {
                 newT[h] = (tA[h] & ~q.oc[s][h]) | (tB[h] & Op[h]);
             }
@@ -197,7 +203,7 @@ __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const 
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            q.oc[s][h] = h < TBD ? D[h] : Op[h];
+            q.oc[s][h] = (h < TBD || (DL & (1 << h))) ? D[h] : Op[h];
             q.lp[s][P2][h] = Lp[h];
             if (s < K - 1) q.nt[s][P3][h] = newT[h];
         }
@@ -231,7 +237,7 @@ __device__ __noinline__ void wide_copy_images(const StepArgs& a, int r_lo, int r
 // cp.async (LDGSTS) into a commit-group ring like step_block_kernel's (false).
 // PITCH: the row pitch in words at compile time (0: StepArgs::pitch), so the
 // unrolled loop addresses its six rows with immediate offsets
-template <int K, int COUNT, bool TMA = true, int MAXT = 256, bool EO = false, int TBD = 0, int PITCH = 0>
+template <int K, int COUNT, bool TMA = true, int MAXT = 256, bool EO = false, int TBD = 0, int PITCH = 0, int DL = 0>
 __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
     static_assert(!(EO && TMA), "the even/odd layout uses the LDGSTS ring");
     if (BML_PDL) {
@@ -357,12 +363,12 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
         using P4 = std::integral_constant<int, 4>;
         using P5 = std::integral_constant<int, 5>;
         for (int j = j_begin; j < j_end; j += 6) {
-            wide_iter<K, COUNT, 0, EO, TBD, PITCH>(q, next_row(P0{}), j, a, c);
-            wide_iter<K, COUNT, 1, EO, TBD, PITCH>(q, next_row(P1{}), j + 1, a, c);
-            wide_iter<K, COUNT, 2, EO, TBD, PITCH>(q, next_row(P2{}), j + 2, a, c);
-            wide_iter<K, COUNT, 3, EO, TBD, PITCH>(q, next_row(P3{}), j + 3, a, c);
-            wide_iter<K, COUNT, 4, EO, TBD, PITCH>(q, next_row(P4{}), j + 4, a, c);
-            wide_iter<K, COUNT, 5, EO, TBD, PITCH>(q, next_row(P5{}), j + 5, a, c);
+            wide_iter<K, COUNT, 0, EO, TBD, PITCH, DL>(q, next_row(P0{}), j, a, c);
+            wide_iter<K, COUNT, 1, EO, TBD, PITCH, DL>(q, next_row(P1{}), j + 1, a, c);
+            wide_iter<K, COUNT, 2, EO, TBD, PITCH, DL>(q, next_row(P2{}), j + 2, a, c);
+            wide_iter<K, COUNT, 3, EO, TBD, PITCH, DL>(q, next_row(P3{}), j + 3, a, c);
+            wide_iter<K, COUNT, 4, EO, TBD, PITCH, DL>(q, next_row(P4{}), j + 4, a, c);
+            wide_iter<K, COUNT, 5, EO, TBD, PITCH, DL>(q, next_row(P5{}), j + 5, a, c);
         }
         // the last kWideRing - 1 issues (rows j_end .. j_end + 4) were never
         // consumed: wait for them so every slot's parity is in step for the next item
