@@ -351,8 +351,15 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
             }
             const uint4 x = ring[wid][P][lane];
             if (TMA) __syncwarp();  // every lane has read slot P before it is refilled
-            issue_to((P + kWideRing - 1) % kWideRing);
+            // EO refills the slot read one iteration earlier AFTER the iteration's
+            // stages (refill_after): the LDS and the LDGSTS are then far apart, and
+            // ptxas needs no padding between them
+            if (!EO) issue_to((P + kWideRing - 1) % kWideRing);
             return x;
+        };
+        auto refill_after = [&](auto p_const) {
+            constexpr int P = decltype(p_const)::value;
+            if (EO) issue_to((P + kWideRing - 1) % kWideRing);
         };
 #pragma unroll
         for (int i = 0; i < kWideRing - 1; ++i) issue_to(i);
@@ -364,11 +371,17 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
         using P5 = std::integral_constant<int, 5>;
         for (int j = j_begin; j < j_end; j += 6) {
             wide_iter<K, COUNT, 0, EO, TBD, PITCH, DL>(q, next_row(P0{}), j, a, c);
+            refill_after(P0{});
             wide_iter<K, COUNT, 1, EO, TBD, PITCH, DL>(q, next_row(P1{}), j + 1, a, c);
+            refill_after(P1{});
             wide_iter<K, COUNT, 2, EO, TBD, PITCH, DL>(q, next_row(P2{}), j + 2, a, c);
+            refill_after(P2{});
             wide_iter<K, COUNT, 3, EO, TBD, PITCH, DL>(q, next_row(P3{}), j + 3, a, c);
+            refill_after(P3{});
             wide_iter<K, COUNT, 4, EO, TBD, PITCH, DL>(q, next_row(P4{}), j + 4, a, c);
+            refill_after(P4{});
             wide_iter<K, COUNT, 5, EO, TBD, PITCH, DL>(q, next_row(P5{}), j + 5, a, c);
+            refill_after(P5{});
         }
         // the last kWideRing - 1 issues (rows j_end .. j_end + 4) were never
         // consumed: wait for them so every slot's parity is in step for the next item
