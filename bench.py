@@ -214,8 +214,8 @@ def abi_check(lib, rc, what):
 KERNEL_MIX = {
     # 4 LOP3 + 2 funnel shifts (+ loop predicates); 1089 instructions / 96 stages
     "step_block_kernel": {"alu": 6.0, "issue": 11.34},
-    # even/odd layout: 3.5 LOP3 + 1 funnel shift (+ address adds); 1582 / 168 stages
-    "step_wide_kernel (even/odd layout)": {"alu": 4.6, "issue": 9.42},
+    # even/odd layout: 3.5 LOP3 + 1 funnel shift (+ loop overhead); 1571 / 168 stages
+    "step_wide_kernel (even/odd layout)": {"alu": 4.6, "issue": 9.35},
     "resident_kernel": {"alu": 6.0, "issue": None},
 }
 KERNEL_NAMES = {1: "step_block_kernel", 2: "step_wide_kernel", 3: "step_wide_kernel (even/odd layout)",
@@ -234,8 +234,8 @@ def alu_roofline(kernel, achieved_gcups, resident_cluster, sm_max_mhz, sms=148):
     (KERNEL_MIX). The narrow kernel issues 6 ALU-pipe instructions per 32-cell
     stage (4 LOP3 + 2 funnel shifts; the ORs of disjoint planes go to the FMA
     pipe): 2/6 x 1024 = 341 cell-updates per clock per SM, below its issue bound.
-    The even/odd-layout kernel needs 4.6 ALU but issues 9.42 instructions per
-    stage, so issue binds: 4/9.42 x 1024 = 435. `achieved` is the dominant
+    The even/odd-layout kernel needs 4.6 ALU but issues 9.35 instructions per
+    stage, so issue binds: 4/9.35 x 1024 = 438. `achieved` is the dominant
     kernel's rate (its event-timed launches), over the SMs it runs on (the
     resident kernel: one cluster)."""
     used = resident_cluster if kernel == "resident_kernel" and resident_cluster else sms

@@ -87,10 +87,22 @@ struct WideCtx {
 // store for a half pair (the lanes next to the ghost words). The even/odd layout
 // only has whole pairs: the 8-byte forms (and the register moves that build
 // their aligned operand pairs) are left out.
-template <bool EO>
+// OFF >= 0 (even/odd layout, compile-time pitch): the row is c.outp + OFF bytes,
+// an immediate offset; the caller advances c.outp once per unrolled loop.
+template <bool EO, int OFF = -1>
 __device__ __forceinline__ void wide_store(const StepArgs& a, WideCtx& c, int o, const uint32_t l[2],
                                            const uint32_t t[2], int pitch) {
     const bool st = static_cast<unsigned>(o - c.r_lo) < c.span;
+    if (EO && OFF >= 0) {
+        asm volatile(
+            "{\n .reg .pred pf;\n"
+            " setp.ne.u32 pf, %0, 0;\n"
+            " @pf st.global.v4.u32 [%1+%6], {%2, %3, %4, %5};\n"
+            "}" ::"r"(static_cast<uint32_t>(st)),
+            "l"(c.outp), "r"(l[0]), "r"(t[0]), "r"(l[1]), "r"(t[1]), "n"(OFF)
+            : "memory");
+        return;
+    }
     if (EO) {
         asm volatile(
             "{\n .reg .pred pf;\n"
@@ -193,7 +205,7 @@ __device__ __forceinline__ void wide_iter(WideState<K>& q, const uint4 x, const 
         }
         if (s == K - 1) {
             const uint32_t* nl = q.lp[s][(P2 + 1) % 2];
-            wide_store<EO>(a, c, j - 2 * K + 1, nl, newT, PITCH ? PITCH : a.pitch);
+            wide_store<EO, (EO && PITCH) ? P * PITCH * 8 : -1>(a, c, j - 2 * K + 1, nl, newT, PITCH ? PITCH : a.pitch);
             if (COUNT == 1) {  // census after the launch's last step: the stored row (branch-free)
                 const bool st = static_cast<unsigned>(j - 2 * K + 1 - c.r_lo) < c.span;
                 const uint32_t add = __popc(nl[0] & c.v0) + __popc(nl[1] & c.v1) +
@@ -359,7 +371,15 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
         };
         auto refill_after = [&](auto p_const) {
             constexpr int P = decltype(p_const)::value;
-            if (EO) issue_to((P + kWideRing - 1) % kWideRing);
+            if (EO && PITCH && !TMA) {  // row gsrc + P rows: an immediate offset, gsrc advances per loop
+                const unsigned sm = ring_base + ((P + kWideRing - 1) % kWideRing) * kSlotBytes + 16u * lane;
+                asm volatile("cp.async.cg.shared.global [%0], [%1+%2], 16;" ::"r"(sm), "l"(gsrc + w0),
+                             "n"(P * PITCH * 8)
+                             : "memory");
+                cp_async_commit();
+            } else if (EO) {
+                issue_to((P + kWideRing - 1) % kWideRing);
+            }
         };
 #pragma unroll
         for (int i = 0; i < kWideRing - 1; ++i) issue_to(i);
@@ -382,6 +402,10 @@ __global__ void __launch_bounds__(MAXT, 1) step_wide_kernel(const StepArgs a) {
             refill_after(P4{});
             wide_iter<K, COUNT, 5, EO, TBD, PITCH, DL>(q, next_row(P5{}), j + 5, a, c);
             refill_after(P5{});
+            if (EO && PITCH) {
+                gsrc += 6 * PITCH;
+                c.outp += 6 * PITCH;
+            }
         }
         // the last kWideRing - 1 issues (rows j_end .. j_end + 4) were never
         // consumed: wait for them so every slot's parity is in step for the next item
