@@ -189,14 +189,16 @@ def load_abi():
     lib.bml_dev_info.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 5 + [ctypes.POINTER(ctypes.c_size_t)]
     lib.bml_dev_last_launch.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 3
     lib.bml_dev_last_kernel.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64)]
+    lib.bml_dev_last_kernel_launch.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 3
     lib.bml_dev_last_error.restype = ctypes.c_char_p
     return lib
 
 
 def last_launch(abi, h):
+    """Geometry of the dominant step kernel's last launch (not a run's short tail)."""
     ns, items, grid = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    abi_check(abi, abi.bml_dev_last_launch(h, ctypes.byref(ns), ctypes.byref(items), ctypes.byref(grid)),
-              "last_launch")
+    abi_check(abi, abi.bml_dev_last_kernel_launch(h, ctypes.byref(ns), ctypes.byref(items), ctypes.byref(grid)),
+              "last_kernel_launch")
     return {"strips": ns.value, "items": items.value, "ctas": grid.value}
 
 

@@ -203,6 +203,11 @@ int bml_dev_set_variant(bml_dev *dev, int variant);
 #define BML_KERNEL_RESIDENT 5
 int bml_dev_last_kernel(bml_dev *dev, int *kernel, int64_t *steps);
 
+/* Launch geometry (row strips, work items, CTAs) of that dominant kernel's last
+ * launch in the last bml_dev_step call (zeros for the resident kernel or no
+ * steps); bml_dev_last_launch reports the very last launch, e.g. a run's tail. */
+int bml_dev_last_kernel_launch(bml_dev *dev, int *nstrips, int *items, int *grid);
+
 /* Geometry of the last streaming-kernel launch: row strips, work items
  * (strips x warp columns) and CTAs. */
 int bml_dev_last_launch(bml_dev *dev, int *nstrips, int *items, int *grid);

@@ -211,6 +211,7 @@ struct bml_dev {
     int resident = 1;        // 1: use the cluster-resident kernel when the lattice qualifies
     int resident_cluster = 0;  // cluster size actually used by the last resident launch
     int last_nstrips = 0, last_grid = 0, last_items = 0;  // last streaming launch
+    int kind_geom[6][3] = {};  // per BML_KERNEL_*: strips, items, grid of its last launch
     long long kernel_steps[6] = {};  // steps per BML_KERNEL_* in the last bml_dev_step call
     int ns_cache_k[kHalo + 1] = {};        // memoised choose_nstrips per block depth
     int ns_cache_setting[kHalo + 1] = {};  // the strip_rows setting it was computed for
@@ -562,9 +563,13 @@ int launch_block(bml_dev* d, int k, bool count, bool census, int step_base, int 
         if (StepKernel narrow = pick_narrow(k, d->mode, metrics)) kern = narrow;
     }
     d->last_nstrips = nstrips;
-    d->kernel_steps[eo ? BML_KERNEL_WIDE_EO : wide ? BML_KERNEL_WIDE : split ? BML_KERNEL_SPLIT : BML_KERNEL_NARROW] += k;
+    const int kind = eo ? BML_KERNEL_WIDE_EO : wide ? BML_KERNEL_WIDE : split ? BML_KERNEL_SPLIT : BML_KERNEL_NARROW;
+    d->kernel_steps[kind] += k;
     d->last_grid = grid;
     d->last_items = a.items;
+    d->kind_geom[kind][0] = nstrips;
+    d->kind_geom[kind][1] = a.items;
+    d->kind_geom[kind][2] = grid;
 
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (d->timing) {
@@ -920,6 +925,17 @@ int bml_dev_last_launch(bml_dev* d, int* nstrips, int* items, int* grid) {
     if (nstrips) *nstrips = d->last_nstrips;
     if (items) *items = d->last_items;
     if (grid) *grid = d->last_grid;
+    return BML_OK;
+}
+
+int bml_dev_last_kernel_launch(bml_dev* d, int* nstrips, int* items, int* grid) {
+    if (!d) return fail(BML_EINVAL, "null bml_dev handle");
+    int kind = BML_KERNEL_NONE;
+    if (int rc = bml_dev_last_kernel(d, &kind, nullptr)) return rc;
+    const bool streaming = kind != BML_KERNEL_NONE && kind != BML_KERNEL_RESIDENT;
+    if (nstrips) *nstrips = streaming ? d->kind_geom[kind][0] : 0;
+    if (items) *items = streaming ? d->kind_geom[kind][1] : 0;
+    if (grid) *grid = streaming ? d->kind_geom[kind][2] : 0;
     return BML_OK;
 }
 

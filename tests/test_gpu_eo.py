@@ -171,3 +171,22 @@ def test_eo_census_reports_the_fault(gpu, strict, want):
         lat.step_with_metrics(150)
     m = re.search(r"conservation violated at step (\d+) of (\d+)", str(ei.value))
     assert m and int(m.group(1)) == want, str(ei.value)
+
+
+def test_dominant_kernel_launch_geometry(gpu):
+    """bml_dev_last_kernel_launch reports the even/odd launches of a 60-step run at
+    N=32768 (65 strips x 18 windows), not the 4-step narrow tail launched last."""
+    lib = ctypes.CDLL(gpu.LIB_DEV)
+    for f in ("bml_dev_last_kernel_launch", "bml_dev_last_launch"):
+        getattr(lib, f).argtypes = [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int)] * 3
+    lat = gpu.DeviceLattice(32768)
+    lat.init_random(0.35, 1)
+    lat.step(60)
+    h = ctypes.c_void_p(lat.handle())
+    dom = [ctypes.c_int() for _ in range(3)]
+    last = [ctypes.c_int() for _ in range(3)]
+    assert lib.bml_dev_last_kernel_launch(h, *[ctypes.byref(x) for x in dom]) == 0
+    assert lib.bml_dev_last_launch(h, *[ctypes.byref(x) for x in last]) == 0
+    assert last_kernel(gpu, lat) == (3, 56)
+    assert dom[1].value == dom[0].value * 18 and dom[2].value == 148
+    assert [x.value for x in dom] != [x.value for x in last]
