@@ -1,8 +1,7 @@
-"""compute-sanitizer target: the pitch-specialised even/odd kernels (N=32768 and 65536
-instantiations are only used at those sizes) for one 60-step run each, digest checked
-against the unmodified reference's golden where one exists at 60 steps (none: the
-digest is printed for the log), plus the N=32768 10000-step golden at the end."""
-import json
+"""compute-sanitizer target: the pitch-specialised even/odd kernel (the N=32768
+instantiation, immediate row offsets, zero pad rows past the band end) for one 60-step
+run on a device-drawn lattice; prints the digest and vehicle counts for the log
+(bit-exactness of that kernel is covered by tests/test_gpu_eo.py's goldens)."""
 import os
 import sys
 
